@@ -1,0 +1,140 @@
+/*
+ * sylkrylov_b200.h -- C-ABI of the B200-native factorized-Krylov hot path.
+ *
+ * Drop-in boundary for the reference's solver entry points
+ * (proj/include/sylkrylov/factorized_solvers.hpp:39-61). Plain pointers and
+ * sizes only; no C++ or torch types. The C++ shim
+ * include/sylkrylov_b200/factorized_solvers.hpp rebuilds the reference's
+ * `sylkrylov::FactorizedSolution` and re-throws its exception types
+ * (errors.hpp:9-57) on top of these functions.
+ *
+ * Threading: one in-flight solve per device; calls are reentrant across
+ * devices. Errors: negative sk_status, message via sk_last_error()
+ * (thread-local), mirroring the reference's exception taxonomy.
+ */
+#ifndef SYLKRYLOV_B200_H
+#define SYLKRYLOV_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* CSR operator, reference index width (sparse_matrix.hpp:11-48: 64-bit
+ * index_t, strictly increasing columns per row). Host pointers unless
+ * sk_gpu_options.inputs_on_device is set. */
+typedef struct {
+    int64_t n_rows, n_cols, nnz;
+    const int64_t* row_ptr;
+    const int64_t* col_idx;
+    const double* values;
+} sk_csr;
+
+/* Field-for-field mirror of SolverConfig (solver_types.hpp:36-45). */
+typedef struct {
+    double eps_tol;              /* default 1e-8 */
+    int64_t max_iter;            /* 0 -> min(10*ceil(sqrt(n*m)), 10000) (solver_types.cpp:34-38) */
+    double breakdown_tol;        /* default 1e-12 */
+    int32_t capture_iterates;    /* test hook: snapshot the core after every iteration */
+    int32_t lanczos_full_reorth; /* forwarded to block Lanczos */
+} sk_config;
+
+/* Device-side options (no reference counterpart). Zero-initialise for defaults. */
+typedef struct {
+    int32_t device;              /* CUDA ordinal */
+    int32_t profile;             /* 1: time every kernel class with CUDA events */
+    int64_t capacity_bytes;      /* HBM budget for the bases (0: 90% of free memory) */
+    int32_t reserved[8];
+} sk_gpu_options;
+
+typedef enum {
+    SK_OK = 0,
+    SK_ERR_DIMENSION = -1,       /* DimensionError         (errors.hpp:9-13)  */
+    SK_ERR_INVALID_MATRIX = -2,  /* InvalidMatrixError     (errors.hpp:18-21) */
+    SK_ERR_RANK_DEFICIENT = -3,  /* RankDeficientStartError(errors.hpp:24-27) */
+    SK_ERR_CUDA = -10,           /* CUDA runtime failure, or no device       */
+    SK_ERR_OUT_OF_MEMORY = -11,
+    SK_ERR_CAPACITY = -12,       /* basis budget exceeded before max_iter    */
+    SK_ERR_UNSUPPORTED = -13     /* e.g. block size s > 8 on the device path */
+} sk_status;
+
+/* SolveStatus (solver_types.hpp:11) */
+enum { SK_SOLVE_CONVERGED = 0, SK_SOLVE_MAX_ITER = 1, SK_SOLVE_BREAKDOWN = 2 };
+
+/* IterationRecord (solver_types.hpp:15-23) */
+typedef struct {
+    int64_t iteration;
+    double rel_residual;
+    double t_basic_s;
+    double t_krylov_s;
+    double t_trunc_s;
+} sk_iteration_record;
+
+/* Execution statistics of one solve (device-timed). */
+typedef struct {
+    double device_time_s;        /* whole solve on the device (events) */
+    double h2d_time_s, d2h_time_s;
+    int64_t h2d_bytes, d2h_bytes;
+    int64_t kernel_launches;
+    int64_t iterations;
+    /* per kernel class (profile=1): 0 spmm, 1 gram, 2 rare-path, 3 write-block,
+     * 4 core-a, 5 core-b, 6 arnoldi-update, 7 dense-image, 8 other */
+    double class_time_s[9];
+    int64_t class_launches[9];
+    double class_bytes[9];       /* algorithmic bytes */
+    int64_t paths[4];            /* extension paths: pythagorean, explicit, householder, clean-up */
+} sk_solve_stats;
+
+typedef struct sk_solution sk_solution;
+
+/* factorized_cg (factorized_solvers.hpp:39-43; factorized_solvers.cpp:204-210) */
+sk_status sk_factorized_cg(const sk_csr* a, const sk_csr* b, const double* c1, const double* c2,
+                           int64_t s, const sk_config* cfg, const sk_gpu_options* gpu,
+                           sk_solution** out);
+/* factorized_cg_lyapunov (factorized_solvers.hpp:45-48; .cpp:212-218) */
+sk_status sk_factorized_cg_lyapunov(const sk_csr* a, const double* c1, int64_t s,
+                                    const sk_config* cfg, const sk_gpu_options* gpu,
+                                    sk_solution** out);
+/* factorized_bicgstab (factorized_solvers.hpp:50-53; .cpp:220-389) */
+sk_status sk_factorized_bicgstab(const sk_csr* a, const sk_csr* b, const double* c1,
+                                 const double* c2, int64_t s, const sk_config* cfg,
+                                 const sk_gpu_options* gpu, sk_solution** out);
+
+/* Resident problems: inputs uploaded once, solved many times (benchmarks). */
+typedef struct sk_problem sk_problem;
+enum { SK_METHOD_CG = 0, SK_METHOD_CG_LYAPUNOV = 1, SK_METHOD_BICGSTAB = 2 };
+sk_status sk_problem_create(int32_t method, const sk_csr* a, const sk_csr* b, const double* c1,
+                            const double* c2, int64_t s, const sk_gpu_options* gpu,
+                            sk_problem** out);
+sk_status sk_problem_solve(sk_problem* p, const sk_config* cfg, sk_solution** out);
+void sk_problem_free(sk_problem* p);
+
+/* FactorizedSolution accessors (factorized_solvers.hpp:14-23). V/core/W stay
+ * in HBM until copied; copies are column-major like DenseMatrix. */
+int32_t sk_solution_status(const sk_solution* sol);
+void sk_solution_dims(const sk_solution* sol, int64_t* n, int64_t* rv, int64_t* m, int64_t* rw);
+int64_t sk_solution_num_records(const sk_solution* sol);
+sk_status sk_solution_history(const sk_solution* sol, sk_iteration_record* records, int64_t count);
+double sk_solution_total_time(const sk_solution* sol);
+sk_status sk_solution_copy_V(const sk_solution* sol, double* out);    /* n  x rv */
+sk_status sk_solution_copy_core(const sk_solution* sol, double* out); /* rv x rw */
+sk_status sk_solution_copy_W(const sk_solution* sol, double* out);    /* m  x rw */
+int64_t sk_solution_num_captured(const sk_solution* sol);
+sk_status sk_solution_captured_core(const sk_solution* sol, int64_t i, int64_t* rows,
+                                    int64_t* cols, double* out);
+sk_status sk_solution_stats(const sk_solution* sol, sk_solve_stats* out);
+void sk_solution_free(sk_solution* sol);
+
+const char* sk_last_error(void);
+const char* sk_version(void);
+int32_t sk_device_count(void);
+
+/* Kernel-level entry for parity tests: y = A x (reference spmm order) or
+ * y = A^T x (spmm_transpose, via the transposed CSR) on the device. */
+sk_status sk_spmm(const sk_csr* a, const double* x, int64_t s, int32_t transpose, double* y);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,391 @@
+"""sylkrylov-b200: B200-native factorized Krylov solvers for AX + XB = C1 C2^T.
+
+Python mirror of the reference interface (proj/include/sylkrylov/
+factorized_solvers.hpp:39-61, solver_types.hpp:11-47, errors.hpp:9-57) over the
+C-ABI in include/sylkrylov_b200.h. The compute path is libsk_b200.so (sm_100a
+kernels); there is no CPU fallback -- loading fails loudly when the library or
+a CUDA device is missing.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass, field
+from typing import List, Optional
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libsk_b200.so")
+
+i64p = C.POINTER(C.c_int64)
+f64p = C.POINTER(C.c_double)
+
+
+# ---- errors (errors.hpp:9-57) ----
+class SylkrylovError(RuntimeError):
+    code = 0
+
+
+class DimensionError(SylkrylovError, ValueError):
+    code = -1
+
+
+class InvalidMatrixError(SylkrylovError, ValueError):
+    code = -2
+
+
+class RankDeficientStartError(SylkrylovError):
+    code = -3
+
+
+class CudaError(SylkrylovError):
+    code = -10
+
+
+class OutOfMemoryError(SylkrylovError, MemoryError):
+    code = -11
+
+
+class CapacityError(SylkrylovError):
+    code = -12
+
+
+class UnsupportedError(SylkrylovError):
+    code = -13
+
+
+_ERRORS = {e.code: e for e in [DimensionError, InvalidMatrixError, RankDeficientStartError,
+                                CudaError, OutOfMemoryError, CapacityError, UnsupportedError]}
+
+
+class _Csr(C.Structure):
+    _fields_ = [("n_rows", C.c_int64), ("n_cols", C.c_int64), ("nnz", C.c_int64),
+                ("row_ptr", i64p), ("col_idx", i64p), ("values", f64p)]
+
+
+class _Cfg(C.Structure):
+    _fields_ = [("eps_tol", C.c_double), ("max_iter", C.c_int64), ("breakdown_tol", C.c_double),
+                ("capture_iterates", C.c_int32), ("lanczos_full_reorth", C.c_int32)]
+
+
+class _Gpu(C.Structure):
+    _fields_ = [("device", C.c_int32), ("profile", C.c_int32), ("capacity_bytes", C.c_int64),
+                ("reserved", C.c_int32 * 8)]
+
+
+class _Rec(C.Structure):
+    _fields_ = [("iteration", C.c_int64), ("rel_residual", C.c_double), ("t_basic_s", C.c_double),
+                ("t_krylov_s", C.c_double), ("t_trunc_s", C.c_double)]
+
+
+class _Stats(C.Structure):
+    _fields_ = [("device_time_s", C.c_double), ("h2d_time_s", C.c_double), ("d2h_time_s", C.c_double),
+                ("h2d_bytes", C.c_int64), ("d2h_bytes", C.c_int64), ("kernel_launches", C.c_int64),
+                ("iterations", C.c_int64), ("class_time_s", C.c_double * 9),
+                ("class_launches", C.c_int64 * 9), ("class_bytes", C.c_double * 9),
+                ("paths", C.c_int64 * 4)]
+
+
+KERNEL_CLASSES = ["spmm", "gram", "rare_path", "write_block", "core_a", "core_b",
+                  "arnoldi_update", "dense_image", "other"]
+
+_lib = None
+
+
+def lib() -> C.CDLL:
+    """Loads libsk_b200.so (build it with `python paper_2605_28274_b200/build.py`)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} missing: run paper_2605_28274_b200/build.py "
+                              "(the B200 path has no CPU fallback)")
+        L = C.CDLL(LIB_PATH)
+        L.sk_last_error.restype = C.c_char_p
+        L.sk_version.restype = C.c_char_p
+        L.sk_solution_total_time.restype = C.c_double
+        for f in ["sk_solution_num_records", "sk_solution_num_captured"]:
+            getattr(L, f).restype = C.c_int64
+        L.sk_solution_status.restype = C.c_int32
+        L.sk_device_count.restype = C.c_int32
+        _lib = L
+    return _lib
+
+
+def _check(rc: int):
+    if rc != 0:
+        raise _ERRORS.get(rc, SylkrylovError)(lib().sk_last_error().decode())
+
+
+def _p(a, t=f64p):
+    return a.ctypes.data_as(t)
+
+
+def device_count() -> int:
+    return int(lib().sk_device_count())
+
+
+# ---- types (sparse_matrix.hpp, solver_types.hpp) ----
+@dataclass
+class SparseMatrix:
+    """CSR with 64-bit indices and strictly increasing columns per row."""
+    n_rows: int
+    n_cols: int
+    row_ptr: np.ndarray
+    col_idx: np.ndarray
+    values: np.ndarray
+
+    @property
+    def nnz(self) -> int:
+        return int(self.values.size)
+
+    def rows(self) -> int:
+        return self.n_rows
+
+    def cols(self) -> int:
+        return self.n_cols
+
+    def _c(self) -> _Csr:
+        self.row_ptr = np.ascontiguousarray(self.row_ptr, dtype=np.int64)
+        self.col_idx = np.ascontiguousarray(self.col_idx, dtype=np.int64)
+        self.values = np.ascontiguousarray(self.values, dtype=np.float64)
+        return _Csr(self.n_rows, self.n_cols, self.nnz, _p(self.row_ptr, i64p),
+                    _p(self.col_idx, i64p), _p(self.values))
+
+    @staticmethod
+    def from_scipy(m) -> "SparseMatrix":
+        m = m.tocsr()
+        m.sort_indices()
+        return SparseMatrix(m.shape[0], m.shape[1], m.indptr.astype(np.int64),
+                            m.indices.astype(np.int64), m.data.astype(np.float64))
+
+    @staticmethod
+    def identity(n: int) -> "SparseMatrix":
+        return SparseMatrix(n, n, np.arange(n + 1, dtype=np.int64), np.arange(n, dtype=np.int64),
+                            np.ones(n))
+
+
+@dataclass
+class SolverConfig:
+    eps_tol: float = 1e-8
+    max_iter: int = 0
+    breakdown_tol: float = 1e-12
+    capture_iterates: bool = False
+    lanczos_full_reorth: bool = False
+
+    def _c(self) -> _Cfg:
+        return _Cfg(self.eps_tol, self.max_iter, self.breakdown_tol, int(self.capture_iterates),
+                    int(self.lanczos_full_reorth))
+
+
+@dataclass
+class GpuOptions:
+    device: int = 0
+    profile: bool = False
+    capacity_bytes: int = 0
+
+    def _c(self) -> _Gpu:
+        return _Gpu(self.device, int(self.profile), self.capacity_bytes)
+
+
+@dataclass
+class IterationRecord:
+    iteration: int
+    rel_residual: float
+    t_basic_s: float = 0.0
+    t_krylov_s: float = 0.0
+    t_trunc_s: float = 0.0
+
+
+@dataclass
+class ConvergenceHistory:
+    records: List[IterationRecord] = field(default_factory=list)
+    total_time_s: float = 0.0
+
+    def iterations(self) -> int:
+        return self.records[-1].iteration if self.records else 0
+
+    def final_rel_residual(self) -> float:
+        return self.records[-1].rel_residual if self.records else 1.0
+
+    def rel_residuals(self) -> np.ndarray:
+        return np.array([r.rel_residual for r in self.records])
+
+
+STATUS = {0: "converged", 1: "max_iter", 2: "breakdown"}
+
+
+class FactorizedSolution:
+    """X = V core W^T (factorized_solvers.hpp:14-23). V, core, W are fetched from
+    HBM lazily (V/W can be tens of GB at the large configs)."""
+
+    def __init__(self, handle):
+        self._h = handle
+        L = lib()
+        self.status = STATUS[int(L.sk_solution_status(handle))]
+        n, rv, m, rw = (C.c_int64() for _ in range(4))
+        L.sk_solution_dims(handle, C.byref(n), C.byref(rv), C.byref(m), C.byref(rw))
+        self.n, self.rv, self.m, self.rw = n.value, rv.value, m.value, rw.value
+        cnt = int(L.sk_solution_num_records(handle))
+        recs = (_Rec * max(cnt, 1))()
+        _check(L.sk_solution_history(handle, recs, C.c_int64(cnt)))
+        self.history = ConvergenceHistory(
+            [IterationRecord(r.iteration, r.rel_residual, r.t_basic_s, r.t_krylov_s, r.t_trunc_s)
+             for r in recs[:cnt]], float(L.sk_solution_total_time(handle)))
+        st = _Stats()
+        _check(L.sk_solution_stats(handle, C.byref(st)))
+        self.stats = {
+            "device_time_s": st.device_time_s, "h2d_time_s": st.h2d_time_s,
+            "h2d_bytes": st.h2d_bytes, "d2h_bytes": st.d2h_bytes,
+            "kernel_launches": st.kernel_launches, "iterations": st.iterations,
+            "classes": {KERNEL_CLASSES[i]: {"time_s": st.class_time_s[i],
+                                             "launches": st.class_launches[i],
+                                             "bytes": st.class_bytes[i]} for i in range(9)},
+            "paths": dict(zip(["pythagorean", "explicit", "householder", "cleanup"], list(st.paths))),
+        }
+        self.captured_cores = []
+        for i in range(int(L.sk_solution_num_captured(handle))):
+            r_, c_ = C.c_int64(), C.c_int64()
+            _check(L.sk_solution_captured_core(handle, C.c_int64(i), C.byref(r_), C.byref(c_), None))
+            buf = np.zeros((r_.value, c_.value), order="F")
+            _check(L.sk_solution_captured_core(handle, C.c_int64(i), C.byref(r_), C.byref(c_), _p(buf)))
+            self.captured_cores.append(buf)
+        self._V = self._W = self._core = None
+
+    @property
+    def V(self) -> np.ndarray:
+        if self._V is None:
+            self._V = np.zeros((self.n, self.rv), order="F")
+            _check(lib().sk_solution_copy_V(self._h, _p(self._V)))
+        return self._V
+
+    @property
+    def W(self) -> np.ndarray:
+        if self._W is None:
+            self._W = np.zeros((self.m, self.rw), order="F")
+            _check(lib().sk_solution_copy_W(self._h, _p(self._W)))
+        return self._W
+
+    @property
+    def core(self) -> np.ndarray:
+        if self._core is None:
+            self._core = np.zeros((self.rv, self.rw), order="F")
+            _check(lib().sk_solution_copy_core(self._h, _p(self._core)))
+        return self._core
+
+    def free(self):
+        if getattr(self, "_h", None):
+            lib().sk_solution_free(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+
+def _mat(c, rows, name) -> np.ndarray:
+    c = np.asfortranarray(np.asarray(c, dtype=np.float64))
+    if c.ndim != 2 or c.shape[0] != rows:
+        raise DimensionError(f"solver: {name} row count must match the operator")
+    return c
+
+
+def factorized_cg(a: SparseMatrix, b: SparseMatrix, c1, c2, cfg: Optional[SolverConfig] = None,
+                  gpu: Optional[GpuOptions] = None) -> FactorizedSolution:
+    """factorized_cg (factorized_solvers.hpp:39-43)."""
+    c1 = _mat(c1, a.n_rows, "C1")
+    c2 = _mat(c2, b.n_rows, "C2")
+    if c1.shape[1] != c2.shape[1] or c1.shape[1] < 1:
+        raise DimensionError("solver: C1 and C2 must have the same positive column count")
+    ca, cb = a._c(), b._c()
+    h = C.c_void_p()
+    cfg_c = (cfg or SolverConfig())._c()
+    gpu_c = (gpu or GpuOptions())._c()
+    _check(lib().sk_factorized_cg(C.byref(ca), C.byref(cb), _p(c1), _p(c2), C.c_int64(c1.shape[1]),
+                                  C.byref(cfg_c), C.byref(gpu_c), C.byref(h)))
+    return FactorizedSolution(h)
+
+
+def factorized_cg_lyapunov(a: SparseMatrix, c1, cfg: Optional[SolverConfig] = None,
+                           gpu: Optional[GpuOptions] = None) -> FactorizedSolution:
+    """factorized_cg_lyapunov (factorized_solvers.hpp:45-48)."""
+    if a.n_rows != a.n_cols:
+        raise DimensionError("factorized_cg_lyapunov: A must be square")
+    c1 = _mat(c1, a.n_rows, "C1")
+    ca = a._c()
+    h = C.c_void_p()
+    cfg_c = (cfg or SolverConfig())._c()
+    gpu_c = (gpu or GpuOptions())._c()
+    _check(lib().sk_factorized_cg_lyapunov(C.byref(ca), _p(c1), C.c_int64(c1.shape[1]),
+                                           C.byref(cfg_c), C.byref(gpu_c), C.byref(h)))
+    return FactorizedSolution(h)
+
+
+def factorized_bicgstab(a: SparseMatrix, b: SparseMatrix, c1, c2,
+                        cfg: Optional[SolverConfig] = None,
+                        gpu: Optional[GpuOptions] = None) -> FactorizedSolution:
+    """factorized_bicgstab (factorized_solvers.hpp:50-53)."""
+    c1 = _mat(c1, a.n_rows, "C1")
+    c2 = _mat(c2, b.n_rows, "C2")
+    if c1.shape[1] != c2.shape[1] or c1.shape[1] < 1:
+        raise DimensionError("solver: C1 and C2 must have the same positive column count")
+    ca, cb = a._c(), b._c()
+    h = C.c_void_p()
+    cfg_c = (cfg or SolverConfig())._c()
+    gpu_c = (gpu or GpuOptions())._c()
+    _check(lib().sk_factorized_bicgstab(C.byref(ca), C.byref(cb), _p(c1), _p(c2),
+                                        C.c_int64(c1.shape[1]), C.byref(cfg_c), C.byref(gpu_c),
+                                        C.byref(h)))
+    return FactorizedSolution(h)
+
+
+METHODS = {"cg": 0, "cg_lyapunov": 1, "bicgstab": 2}
+
+
+class ResidentProblem:
+    """Inputs uploaded once to HBM (sk_problem_create), solved repeatedly."""
+
+    def __init__(self, method: str, a: SparseMatrix, b: Optional[SparseMatrix], c1, c2=None,
+                 gpu: Optional[GpuOptions] = None):
+        c1 = _mat(c1, a.n_rows, "C1")
+        self._keep = [c1]
+        ca = a._c()
+        cb = b._c() if b is not None else None
+        c2a = _mat(c2, b.n_rows, "C2") if c2 is not None else None
+        self._keep.append(c2a)
+        gpu_c = (gpu or GpuOptions())._c()
+        h = C.c_void_p()
+        _check(lib().sk_problem_create(C.c_int32(METHODS[method]), C.byref(ca),
+                                       C.byref(cb) if cb is not None else None, _p(c1),
+                                       _p(c2a) if c2a is not None else None,
+                                       C.c_int64(c1.shape[1]), C.byref(gpu_c), C.byref(h)))
+        self._h = h
+
+    def solve(self, cfg: Optional[SolverConfig] = None) -> FactorizedSolution:
+        h = C.c_void_p()
+        cfg_c = (cfg or SolverConfig())._c()
+        _check(lib().sk_problem_solve(self._h, C.byref(cfg_c), C.byref(h)))
+        return FactorizedSolution(h)
+
+    def free(self):
+        if getattr(self, "_h", None):
+            lib().sk_problem_free(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+
+def spmm(a: SparseMatrix, x, transpose: bool = False) -> np.ndarray:
+    """Device SpMM (K1) in the reference's per-row order (sparse_matrix.cpp:142-200)."""
+    x = np.asfortranarray(np.asarray(x, dtype=np.float64))
+    rows = a.n_cols if transpose else a.n_rows
+    y = np.zeros((rows, x.shape[1]), order="F")
+    ca = a._c()
+    _check(lib().sk_spmm(C.byref(ca), _p(x), C.c_int64(x.shape[1]), C.c_int32(int(transpose)), _p(y)))
+    return y

@@ -1,0 +1,69 @@
+"""Builds libsk_b200.so (sm_100a) in-tree with nvcc.
+
+Flags: -gencode arch=compute_100a,code=sm_100a -lineinfo -O3 --fmad=false.
+--fmad=false is part of the arithmetic contract: no implicit FMA contraction,
+so the device results are bitwise identical to oracle/ (SKO_REPRODUCIBLE).
+The kernels are instantiated per block size s in separate translation units
+(compiled in parallel).
+"""
+import os
+import subprocess
+import sys
+from concurrent.futures import ThreadPoolExecutor
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+CSRC = os.path.join(HERE, "csrc")
+LIB = os.path.join(HERE, "libsk_b200.so")
+NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+FLAGS = ARCH + ["-lineinfo", "-O3", "--fmad=false", "-std=c++17", "-Xcompiler", "-fPIC",
+                "-Xcompiler", "-Wall", "--expt-relaxed-constexpr",
+                "-I" + os.path.join(HERE, "..", "include")]
+S_VALUES = range(1, 9)
+
+
+def units():
+    u = [("sk_kernels.cu", f"sk_kernels_s{s}.o", [f"-DSK_INST_S={s}"]) for s in S_VALUES]
+    u.append(("sk_kernels.cu", "sk_kernels_common.o", ["-DSK_INST_COMMON"]))
+    u.append(("sk_driver.cu", "sk_driver.o", []))
+    return u
+
+
+def needs_build() -> bool:
+    if not os.path.exists(LIB):
+        return True
+    t = os.path.getmtime(LIB)
+    deps = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if not f.endswith(".o")]
+    deps.append(os.path.join(HERE, "..", "include", "sylkrylov_b200.h"))
+    deps.append(os.path.abspath(__file__))
+    return any(os.path.getmtime(d) > t for d in deps)
+
+
+def _compile(unit, verbose):
+    src, obj, defs = unit
+    cmd = [NVCC, *FLAGS, *defs, "-c", os.path.join(CSRC, src), "-o", os.path.join(CSRC, obj)]
+    if verbose:
+        cmd.insert(1, "-Xptxas=-v")
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(f"nvcc failed for {obj}:\n{r.stderr}")
+    return r.stderr
+
+
+def build(force: bool = False, verbose: bool = False) -> str:
+    if not force and not needs_build():
+        return LIB
+    us = units()
+    with ThreadPoolExecutor(max_workers=min(len(us), os.cpu_count() or 4)) as ex:
+        logs = list(ex.map(lambda u: _compile(u, verbose), us))
+    if verbose:
+        for lg in logs:
+            sys.stderr.write(lg)
+    objs = [os.path.join(CSRC, u[1]) for u in us]
+    subprocess.check_call([NVCC, "-shared", *ARCH, *objs, "-o", LIB + ".tmp", "-lcudart"])
+    os.replace(LIB + ".tmp", LIB)
+    return LIB
+
+
+if __name__ == "__main__":
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))

@@ -1,0 +1,865 @@
+// sk_driver.cu -- host driver + C-ABI of the B200 factorized-Krylov path
+// (include/sylkrylov_b200.h). Host code only; kernels live in sk_kernels.cu.
+//
+// The iteration loop is device-resident: every kernel reads its shapes and the
+// solver status from the DevState in HBM, so the host only enqueues work and
+// polls a pinned status word asynchronously (no host round-trip inside an
+// iteration). Restates the control flow of factorized_solvers.cpp:89-200.
+#include "../../include/sylkrylov_b200.h"
+#include "sk_device.cuh"
+#include "sk_launch.h"
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+namespace {
+
+thread_local std::string g_err;
+
+struct SkError : std::runtime_error {
+  sk_status code;
+  SkError(sk_status c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+#define CK(x)                                                                              \
+  do {                                                                                     \
+    cudaError_t e_ = (x);                                                                  \
+    if (e_ != cudaSuccess)                                                                 \
+      throw SkError(e_ == cudaErrorMemoryAllocation ? SK_ERR_OUT_OF_MEMORY : SK_ERR_CUDA, \
+                    std::string(#x) + ": " + cudaGetErrorString(e_));                      \
+  } while (0)
+
+// ---------------------------------------------------------------------------
+// Host CSR helpers (sparse_matrix.cpp:12-32 validation, :80-95 transpose,
+// :109-132 symmetry)
+// ---------------------------------------------------------------------------
+struct HostCsr {
+  int64_t n_rows = 0, n_cols = 0;
+  std::vector<int64_t> rp, ci;
+  std::vector<double> val;
+};
+
+void validate_csr(const sk_csr* a, const char* what) {
+  if (!a || !a->row_ptr || (a->nnz > 0 && (!a->col_idx || !a->values)))
+    throw SkError(SK_ERR_INVALID_MATRIX, std::string(what) + ": null CSR");
+  if (a->n_rows < 0 || a->n_cols < 0) throw SkError(SK_ERR_INVALID_MATRIX, "SparseMatrix: negative dimension");
+  if (a->row_ptr[0] != 0 || a->row_ptr[a->n_rows] != a->nnz)
+    throw SkError(SK_ERR_INVALID_MATRIX, "SparseMatrix: row_ptr endpoints inconsistent with nnz");
+  for (int64_t i = 0; i < a->n_rows; ++i) {
+    if (a->row_ptr[i] > a->row_ptr[i + 1])
+      throw SkError(SK_ERR_INVALID_MATRIX, "SparseMatrix: row_ptr not nondecreasing");
+    for (int64_t k = a->row_ptr[i]; k < a->row_ptr[i + 1]; ++k) {
+      if (a->col_idx[k] < 0 || a->col_idx[k] >= a->n_cols)
+        throw SkError(SK_ERR_INVALID_MATRIX, "SparseMatrix: column index out of range");
+      if (k > a->row_ptr[i] && a->col_idx[k] <= a->col_idx[k - 1])
+        throw SkError(SK_ERR_INVALID_MATRIX, "SparseMatrix: column indices not strictly increasing in row");
+    }
+  }
+}
+
+HostCsr transpose(const sk_csr* a) {
+  HostCsr t;
+  t.n_rows = a->n_cols;
+  t.n_cols = a->n_rows;
+  t.rp.assign(a->n_cols + 1, 0);
+  t.ci.resize(a->nnz);
+  t.val.resize(a->nnz);
+  for (int64_t k = 0; k < a->nnz; ++k) t.rp[a->col_idx[k] + 1]++;
+  for (int64_t i = 1; i <= a->n_cols; ++i) t.rp[i] += t.rp[i - 1];
+  std::vector<int64_t> next(t.rp.begin(), t.rp.end() - 1);
+  for (int64_t i = 0; i < a->n_rows; ++i)
+    for (int64_t k = a->row_ptr[i]; k < a->row_ptr[i + 1]; ++k) {
+      const int64_t pos = next[a->col_idx[k]]++;
+      t.ci[pos] = i;
+      t.val[pos] = a->values[k];
+    }
+  return t;
+}
+
+bool is_symmetric(const sk_csr* a, double tol) {
+  if (a->n_rows != a->n_cols) return false;
+  HostCsr at = transpose(a);
+  double diff2 = 0.0, fro = 0.0;
+  for (int64_t k = 0; k < a->nnz; ++k) fro += a->values[k] * a->values[k];
+  for (int64_t i = 0; i < a->n_rows; ++i) {
+    int64_t ka = a->row_ptr[i], kb = at.rp[i];
+    const int64_t ea = a->row_ptr[i + 1], eb = at.rp[i + 1];
+    while (ka < ea || kb < eb) {
+      const int64_t ca = ka < ea ? a->col_idx[ka] : a->n_cols;
+      const int64_t cb = kb < eb ? at.ci[kb] : a->n_cols;
+      double d;
+      if (ca < cb)
+        d = a->values[ka++];
+      else if (cb < ca)
+        d = -at.val[kb++];
+      else
+        d = a->values[ka++] - at.val[kb++];
+      diff2 += d * d;
+    }
+  }
+  return std::sqrt(diff2) <= tol * std::max(std::sqrt(fro), 1e-300);
+}
+
+// ---------------------------------------------------------------------------
+// Device CSR (int32 indices: every n, nnz of the configs is < 2^31)
+// ---------------------------------------------------------------------------
+struct DevCsr {
+  int64_t n = 0, nnz = 0;
+  int32_t* rp = nullptr;
+  int32_t* ci = nullptr;
+  double* val = nullptr;
+};
+
+size_t upload_csr(DevCsr& d, int64_t n, int64_t nnz, const int64_t* rp, const int64_t* ci,
+                  const double* val, cudaStream_t st) {
+  if (n >= (int64_t(1) << 31) || nnz >= (int64_t(1) << 31))
+    throw SkError(SK_ERR_UNSUPPORTED, "device CSR uses int32 indices: n and nnz must be < 2^31");
+  std::vector<int32_t> rp32(n + 1), ci32(std::max<int64_t>(nnz, 1));
+  for (int64_t i = 0; i <= n; ++i) rp32[i] = (int32_t)rp[i];
+  for (int64_t k = 0; k < nnz; ++k) ci32[k] = (int32_t)ci[k];
+  d.n = n;
+  d.nnz = nnz;
+  CK(cudaMalloc(&d.rp, sizeof(int32_t) * (n + 1)));
+  CK(cudaMalloc(&d.ci, sizeof(int32_t) * std::max<int64_t>(nnz, 1)));
+  CK(cudaMalloc(&d.val, sizeof(double) * std::max<int64_t>(nnz, 1)));
+  CK(cudaMemcpyAsync(d.rp, rp32.data(), sizeof(int32_t) * (n + 1), cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(d.ci, ci32.data(), sizeof(int32_t) * nnz, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(d.val, val, sizeof(double) * nnz, cudaMemcpyHostToDevice, st));
+  CK(cudaStreamSynchronize(st));  // host staging vectors go out of scope
+  return sizeof(int32_t) * (n + 1 + nnz) + sizeof(double) * nnz;
+}
+void free_csr(DevCsr& d) {
+  cudaFree(d.rp);
+  cudaFree(d.ci);
+  cudaFree(d.val);
+  d = DevCsr();
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// Problem: resident inputs
+// ---------------------------------------------------------------------------
+struct sk_problem {
+  int method = 0;
+  int64_t s = 0, n = 0, m = 0;
+  int device = 0;
+  int profile = 0;
+  int64_t capacity_bytes = 0;
+  DevCsr op[2];  // side 0: A (V basis), side 1: B^T (W basis)
+  double* c1 = nullptr;
+  double* c2 = nullptr;
+  cudaStream_t stream = nullptr;
+  int64_t h2d_bytes = 0;
+  double h2d_time = 0.0;
+};
+
+// ---------------------------------------------------------------------------
+// Solution
+// ---------------------------------------------------------------------------
+struct sk_solution {
+  int32_t status = SK_SOLVE_MAX_ITER;
+  int64_t n = 0, m = 0, rv = 0, rw = 0, s = 0;
+  bool lyap = false;
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  std::vector<sk_iteration_record> hist;
+  std::vector<std::vector<double>> captured;
+  std::vector<std::pair<int64_t, int64_t>> cap_shape;
+  double total_time = 0.0;
+  sk_solve_stats stats{};
+  std::vector<double*> vblocks, wblocks;  // block pointers (row-interleaved n x s)
+  std::vector<double*> chunks;            // owned allocations
+  double* X = nullptr;                    // owned core buffer
+  int64_t ld = 0;
+};
+
+namespace {
+
+int64_t resolve_max_iter(const sk_config& c, int64_t n, int64_t m) {
+  if (c.max_iter > 0) return c.max_iter;
+  const double root = std::sqrt((double)n * (double)m);
+  return std::min<int64_t>(10 * (int64_t)std::ceil(root), 10000);
+}
+
+struct SideBuf {
+  int64_t n = 0;
+  double *w = nullptr, *wx = nullptr, *qh = nullptr, *hw = nullptr;
+  double *hband = nullptr, *coef = nullptr, *coef2 = nullptr, *part = nullptr;
+  unsigned int* counter = nullptr;
+  double** table = nullptr;
+  double** table_host = nullptr;  // pinned mirror (async uploads)
+  std::vector<double*> blocks;
+  int64_t cap_blocks = 0, hld = 0;
+};
+
+struct Solver {
+  sk_problem& P;
+  sk_config cfg;
+  cudaStream_t st;
+  int64_t s, max_iter, cap_blocks;
+  int nsides;
+  bool lyap, arnoldi;
+  SideBuf side[2];
+  std::vector<double*> chunks;
+  // cores
+  int64_t rcap = 0;
+  double *X = nullptr, *R = nullptr, *P0 = nullptr, *P1 = nullptr, *cpart = nullptr;
+  unsigned int* ccounter = nullptr;
+  double *hist_rel = nullptr, *hist_tk = nullptr, *hist_tb = nullptr;
+  sk::DevState* dstate = nullptr;
+  sk::SolveConst c{};
+  // profiling
+  struct Ev {
+    cudaEvent_t a, b;
+    int cls;
+    double bytes;
+  };
+  std::vector<Ev> pending;
+  std::vector<cudaEvent_t> pool;
+  sk_solve_stats stats{};
+
+  explicit Solver(sk_problem& p, const sk_config& cf) : P(p), cfg(cf), st(p.stream) {}
+
+  template <class T>
+  T* dalloc(size_t count, bool zero = true) {
+    void* ptr = nullptr;
+    CK(cudaMallocAsync(&ptr, sizeof(T) * std::max<size_t>(count, 1), st));
+    if (zero) CK(cudaMemsetAsync(ptr, 0, sizeof(T) * std::max<size_t>(count, 1), st));
+    return (T*)ptr;
+  }
+  void dfree(void* p) {
+    if (p) cudaFreeAsync(p, st);
+  }
+
+  cudaEvent_t ev_get() {
+    if (!pool.empty()) {
+      cudaEvent_t e = pool.back();
+      pool.pop_back();
+      return e;
+    }
+    cudaEvent_t e;
+    CK(cudaEventCreate(&e));
+    return e;
+  }
+
+  template <class F>
+  void timed(int cls, double bytes, F&& f) {
+    if (!P.profile) {
+      f();
+      return;
+    }
+    Ev e{ev_get(), ev_get(), cls, bytes};
+    CK(cudaEventRecord(e.a, st));
+    f();
+    CK(cudaEventRecord(e.b, st));
+    pending.push_back(e);
+  }
+  void drain_events(bool all) {
+    size_t keep = all ? 0 : 64;
+    while (pending.size() > keep) {
+      Ev e = pending.front();
+      pending.erase(pending.begin());
+      CK(cudaEventSynchronize(e.b));
+      float ms = 0.f;
+      CK(cudaEventElapsedTime(&ms, e.a, e.b));
+      stats.class_time_s[e.cls] += ms * 1e-3;
+      stats.class_launches[e.cls] += 1;
+      stats.class_bytes[e.cls] += e.bytes;
+      pool.push_back(e.a);
+      pool.push_back(e.b);
+    }
+  }
+
+  void setup() {
+    s = P.s;
+    lyap = P.method == SK_METHOD_CG_LYAPUNOV;
+    arnoldi = P.method == SK_METHOD_BICGSTAB;
+    nsides = lyap ? 1 : 2;
+    max_iter = resolve_max_iter(cfg, P.n, lyap ? P.n : P.m);
+    cap_blocks = arnoldi ? 2 * max_iter + 3 : max_iter + 2;
+    c = sk::SolveConst{};
+    c.nsides = nsides;
+    c.lyap = lyap;
+    c.arnoldi = arnoldi;
+    c.full_reorth = cfg.lanczos_full_reorth;
+    c.s = (int)s;
+    c.tol = cfg.breakdown_tol;
+    c.eps = cfg.eps_tol;
+    c.max_iter = max_iter;
+    for (int sd = 0; sd < nsides; ++sd) {
+      SideBuf& b = side[sd];
+      const DevCsr& op = P.op[sd];
+      b.n = op.n;
+      const int64_t ns = b.n * s;
+      const int64_t ncta = (b.n + sk::kRowsPerCta - 1) / sk::kRowsPerCta;
+      const int64_t nseg = (b.n + sk::kSeg - 1) / sk::kSeg;
+      b.w = dalloc<double>(ns);
+      b.wx = dalloc<double>(ns);
+      b.qh = dalloc<double>(ns);
+      b.hw = dalloc<double>(ns);
+      b.cap_blocks = cap_blocks;
+      if (!arnoldi) {
+        b.hband = dalloc<double>((cap_blocks + 1) * 3 * s * s);
+      }
+      b.coef = dalloc<double>(cap_blocks * s * s);
+      b.coef2 = dalloc<double>(cap_blocks * s * s);
+      b.part = dalloc<double>(std::max<int64_t>((cap_blocks + 3) * ncta * s * s, nseg + 64));
+      b.counter = dalloc<unsigned int>(cap_blocks + 8);
+      b.table = dalloc<double*>(cap_blocks);
+      CK(cudaHostAlloc(&b.table_host, sizeof(double*) * cap_blocks, cudaHostAllocDefault));
+      sk::SideConst& sc = c.side[sd];
+      sc.n = b.n;
+      sc.rp = op.rp;
+      sc.ci = op.ci;
+      sc.val = op.val;
+      sc.blocks = b.table;
+      sc.w = b.w;
+      sc.wx = b.wx;
+      sc.qh = b.qh;
+      sc.hw = b.hw;
+      sc.hband = b.hband;
+      sc.hld = b.hld;
+      sc.coef = b.coef;
+      sc.coef2 = b.coef2;
+      sc.part = b.part;
+      sc.counter = b.counter;
+      sc.ncta = ncta;
+      sc.nseg = nseg;
+    }
+    if (nsides == 1) c.side[1] = c.side[0];
+    dstate = dalloc<sk::DevState>(1);
+    hist_rel = dalloc<double>(max_iter + 2);
+    hist_tk = dalloc<double>(max_iter + 2);
+    hist_tb = dalloc<double>(max_iter + 2);
+    c.hist_rel = hist_rel;
+    c.hist_tk = hist_tk;
+    c.hist_tb = hist_tb;
+    c.st = dstate;
+    grow_cores(std::min<int64_t>((max_iter + 2) * s, 512));
+  }
+
+  void grow_cores(int64_t need) {
+    if (need <= rcap) return;
+    int64_t ncap = std::max<int64_t>(need, 2 * rcap);
+    ncap = std::min<int64_t>(ncap, ((max_iter + 2) * s + 31) / 32 * 32 + 32);
+    ncap = std::max<int64_t>(ncap, need);
+    ncap = (ncap + 31) / 32 * 32;
+    auto grow = [&](double*& buf) {
+      double* nb = dalloc<double>(ncap * ncap);
+      if (buf) {
+        CK(cudaMemcpy2DAsync(nb, ncap * sizeof(double), buf, rcap * sizeof(double),
+                             rcap * sizeof(double), rcap, cudaMemcpyDeviceToDevice, st));
+        dfree(buf);
+      }
+      buf = nb;
+    };
+    grow(X);
+    grow(R);
+    grow(P0);
+    grow(P1);
+    dfree(cpart);
+    dfree(ccounter);
+    const int64_t nt = ncap / 32;
+    cpart = dalloc<double>(nt * nt + nt + 64);
+    ccounter = dalloc<unsigned int>(8);
+    rcap = ncap;
+    c.X = X;
+    c.R = R;
+    c.P[0] = P0;
+    c.P[1] = P1;
+    c.ld = rcap;
+    c.cpart = cpart;
+    c.ccounter = ccounter;
+  }
+
+  void ensure_blocks(int sd, int64_t need) {
+    SideBuf& b = side[sd];
+    if ((int64_t)b.blocks.size() >= need) return;
+    if (need > b.cap_blocks) throw SkError(SK_ERR_CAPACITY, "basis capacity exceeded");
+    const int64_t bb = b.n * s * (int64_t)sizeof(double);
+    int64_t per = std::max<int64_t>(1, (int64_t(1) << 30) / std::max<int64_t>(bb, 1));
+    per = std::min<int64_t>(per, b.cap_blocks - (int64_t)b.blocks.size());
+    per = std::max<int64_t>(per, need - (int64_t)b.blocks.size());
+    double* chunk = dalloc<double>(per * b.n * s, false);
+    chunks.push_back(chunk);
+    const size_t first = b.blocks.size();
+    for (int64_t j = 0; j < per; ++j) {
+      b.blocks.push_back(chunk + j * b.n * s);
+      b.table_host[first + j] = b.blocks.back();
+    }
+    // pinned source entries are written once, so the upload stays asynchronous
+    CK(cudaMemcpyAsync(b.table + first, b.table_host + first, sizeof(double*) * per,
+                       cudaMemcpyHostToDevice, st));
+  }
+
+  double spmm_bytes() const {
+    double b = 0;
+    for (int sd = 0; sd < nsides; ++sd)
+      b += 12.0 * P.op[sd].nnz + 4.0 * (P.op[sd].n + 1) + 16.0 * P.op[sd].n * s;
+    return b;
+  }
+  double pass_bytes(int64_t k, int extra) const {
+    const double J = (double)std::min<int64_t>(k + 1, 2);
+    double b = 0;
+    for (int sd = 0; sd < nsides; ++sd) b += 8.0 * P.op[sd].n * s * (J + extra);
+    return b;
+  }
+
+  sk_solution* run() {
+    setup();
+    cudaEvent_t t0, t1;
+    CK(cudaEventCreate(&t0));
+    CK(cudaEventCreate(&t1));
+    sk::launch_count_reset();
+    for (int sd = 0; sd < nsides; ++sd) ensure_blocks(sd, 1);
+    CK(cudaEventRecord(t0, st));
+    sk::launch_init(c, P.c1, lyap ? P.c1 : P.c2, st);
+    int32_t status = 0;
+    CK(cudaMemcpyAsync(&status, &dstate->status, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    CK(cudaGetLastError());
+    if (status == sk::RANKDEF) {
+      release(nullptr);
+      throw SkError(SK_ERR_RANK_DEFICIENT, "basis init: start block is numerically rank deficient");
+    }
+    // pinned status ring for asynchronous polling
+    const int RING = 64;
+    int32_t* hstat = nullptr;
+    CK(cudaHostAlloc(&hstat, sizeof(int32_t) * RING, cudaHostAllocDefault));
+    std::vector<cudaEvent_t> rev(RING);
+    for (auto& e : rev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    int64_t enq = 0, checked = 0;
+    bool done = false;
+    std::vector<std::vector<double>> caps;
+    std::vector<std::pair<int64_t, int64_t>> cap_shape;
+    for (int64_t k = 0; k < max_iter && !done; ++k) {
+      for (int sd = 0; sd < nsides; ++sd) ensure_blocks(sd, k + 2);
+      grow_cores((k + 2) * s);
+      const double rp = (double)((k + 1) * s), rq = (double)((k + 2) * s);
+      timed(0, spmm_bytes(), [&] { sk::launch_spmm(c, st); });
+      timed(1, pass_bytes(k, 1), [&] { sk::launch_gram_lanczos(c, st); });
+      timed(2, 0.0, [&] { sk::launch_rare(c, k + 1, st); });
+      timed(3, pass_bytes(k, 2), [&] { sk::launch_pass2(c, st); });
+      timed(4, 8.0 * 3 * rp * rp, [&] { sk::launch_cg_a(c, (k + 1) * s, st); });
+      timed(5, 8.0 * (4 * rp * rp + rq * rq), [&] { sk::launch_cg_b(c, (k + 2) * s, st); });
+      CK(cudaMemcpyAsync(&hstat[k % RING], &dstate->status, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+      CK(cudaEventRecord(rev[k % RING], st));
+      enq = k + 1;
+      if (cfg.capture_iterates) {
+        CK(cudaStreamSynchronize(st));
+        sk::DevState hs;
+        CK(cudaMemcpy(&hs, dstate, sizeof hs, cudaMemcpyDeviceToHost));
+        if (hs.status == sk::RUNNING || hs.status == sk::CONVERGED || hs.status == sk::MAXITER) {
+          if (hs.k == k + 1) {
+            std::vector<double> xs(hs.rows_x * hs.cols_x);
+            if (!xs.empty())
+              CK(cudaMemcpy2D(xs.data(), hs.rows_x * sizeof(double), X, rcap * sizeof(double),
+                              hs.rows_x * sizeof(double), hs.cols_x, cudaMemcpyDeviceToHost));
+            caps.push_back(std::move(xs));
+            cap_shape.push_back({hs.rows_x, hs.cols_x});
+          }
+        }
+      }
+      // asynchronous status polling (bounded run-ahead)
+      while (checked < enq) {
+        cudaError_t q = cudaEventQuery(rev[checked % RING]);
+        if (q == cudaErrorNotReady) {
+          if (enq - checked >= RING - 8) {
+            CK(cudaEventSynchronize(rev[checked % RING]));
+            continue;
+          }
+          break;
+        }
+        CK(q);
+        if (hstat[checked % RING] != sk::RUNNING) {
+          done = true;
+          break;
+        }
+        ++checked;
+      }
+      if (P.profile) drain_events(false);
+    }
+    CK(cudaEventRecord(t1, st));
+    CK(cudaStreamSynchronize(st));
+    CK(cudaGetLastError());
+    if (P.profile) drain_events(true);
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, t0, t1));
+    cudaEventDestroy(t0);
+    cudaEventDestroy(t1);
+    for (auto& e : rev) cudaEventDestroy(e);
+    cudaFreeHost(hstat);
+    for (auto e : pool) cudaEventDestroy(e);
+    pool.clear();
+
+    auto* sol = new sk_solution();
+    sol->captured = std::move(caps);
+    sol->cap_shape = std::move(cap_shape);
+    sk::DevState hs;
+    CK(cudaMemcpy(&hs, dstate, sizeof hs, cudaMemcpyDeviceToHost));
+    const int64_t nrec = hs.nrec;
+    std::vector<double> rel(nrec), tk(nrec), tb(nrec);
+    CK(cudaMemcpy(rel.data(), hist_rel, sizeof(double) * nrec, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(tk.data(), hist_tk, sizeof(double) * nrec, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(tb.data(), hist_tb, sizeof(double) * nrec, cudaMemcpyDeviceToHost));
+    sol->hist.resize(nrec);
+    for (int64_t i = 0; i < nrec; ++i) {
+      sk_iteration_record& r = sol->hist[i];
+      r.iteration = i;
+      r.rel_residual = rel[i];
+      r.t_trunc_s = 0.0;
+      if (i == 0) {
+        r.t_basic_s = r.t_krylov_s = 0.0;
+      } else {
+        r.t_krylov_s = std::max(0.0, (tk[i] - tb[i - 1]) * 1e-9);
+        r.t_basic_s = std::max(0.0, (tb[i] - tk[i]) * 1e-9);
+      }
+    }
+    switch (hs.status) {
+      case sk::CONVERGED: sol->status = SK_SOLVE_CONVERGED; break;
+      case sk::BREAKDOWN: sol->status = SK_SOLVE_BREAKDOWN; break;
+      default: sol->status = SK_SOLVE_MAX_ITER; break;
+    }
+    sol->n = P.n;
+    sol->m = lyap ? P.n : P.m;
+    sol->s = s;
+    sol->lyap = lyap;
+    sol->rv = hs.rows_x;
+    sol->rw = hs.cols_x;
+    sol->device = P.device;
+    sol->stream = nullptr;  // legacy stream: the problem's stream may be destroyed first
+    sol->total_time = ms * 1e-3;
+    stats.device_time_s = ms * 1e-3;
+    stats.kernel_launches = sk::launch_count();
+    stats.iterations = nrec - 1;
+    for (int i = 0; i < 4; ++i)
+      for (int sd = 0; sd < nsides; ++sd) stats.paths[i] += hs.side[sd].paths[i];
+    stats.h2d_bytes = P.h2d_bytes;
+    stats.h2d_time_s = P.h2d_time;
+    stats.d2h_bytes = (int64_t)(sizeof(double) * 3 * nrec + sizeof hs);
+    sol->stats = stats;
+    release(sol);
+    return sol;
+  }
+
+  // free everything except what the solution keeps (blocks + X)
+  void release(sk_solution* sol) {
+    for (int sd = 0; sd < nsides; ++sd) {
+      SideBuf& b = side[sd];
+      dfree(b.w);
+      dfree(b.wx);
+      dfree(b.qh);
+      dfree(b.hw);
+      dfree(b.hband);
+      dfree(b.coef);
+      dfree(b.coef2);
+      dfree(b.part);
+      dfree(b.counter);
+      dfree(b.table);
+    }
+    cudaStreamSynchronize(st);
+    for (int sd = 0; sd < nsides; ++sd)
+      if (side[sd].table_host) cudaFreeHost(side[sd].table_host);
+    dfree(R);
+    dfree(P0);
+    dfree(P1);
+    dfree(cpart);
+    dfree(ccounter);
+    dfree(hist_rel);
+    dfree(hist_tk);
+    dfree(hist_tb);
+    dfree(dstate);
+    if (sol) {
+      sol->chunks = chunks;
+      sol->X = X;
+      sol->ld = rcap;
+      const int64_t vb = sol->rv / s, wb = sol->rw / s;
+      sol->vblocks.assign(side[0].blocks.begin(), side[0].blocks.begin() + std::min<int64_t>(vb, side[0].blocks.size()));
+      const SideBuf& w = side[nsides > 1 ? 1 : 0];
+      sol->wblocks.assign(w.blocks.begin(), w.blocks.begin() + std::min<int64_t>(wb, w.blocks.size()));
+    } else {
+      for (double* p : chunks) dfree(p);
+      dfree(X);
+    }
+    cudaStreamSynchronize(st);
+  }
+};
+
+template <class F>
+sk_status run_guarded(F&& f) {
+  try {
+    f();
+    return SK_OK;
+  } catch (const SkError& e) {
+    g_err = e.what();
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    g_err = "host out of memory";
+    return SK_ERR_OUT_OF_MEMORY;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return SK_ERR_CUDA;
+  }
+}
+
+void check_device(int dev) {
+  int count = 0;
+  if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0)
+    throw SkError(SK_ERR_CUDA, "no CUDA device available (the B200 path has no CPU fallback)");
+  if (dev < 0 || dev >= count) throw SkError(SK_ERR_CUDA, "invalid device ordinal");
+  CK(cudaSetDevice(dev));
+}
+
+sk_problem* create_problem(int32_t method, const sk_csr* a, const sk_csr* b, const double* c1,
+                           const double* c2, int64_t s, const sk_gpu_options* gpu) {
+  validate_csr(a, "A");
+  const bool lyap = method == SK_METHOD_CG_LYAPUNOV;
+  if (lyap) {
+    if (a->n_rows != a->n_cols) throw SkError(SK_ERR_DIMENSION, "factorized_cg_lyapunov: A must be square");
+    if (!is_symmetric(a, 1e-12)) throw SkError(SK_ERR_INVALID_MATRIX, "factorized_cg_lyapunov: A is not symmetric");
+  } else {
+    validate_csr(b, "B");
+    if (a->n_rows != a->n_cols || b->n_rows != b->n_cols)
+      throw SkError(SK_ERR_DIMENSION, "solver: A and B must be square");
+    if (s < 1) throw SkError(SK_ERR_DIMENSION, "solver: C1 and C2 must have the same positive column count");
+    if (method == SK_METHOD_CG) {
+      if (!is_symmetric(a, 1e-12)) throw SkError(SK_ERR_INVALID_MATRIX, "factorized_cg: A is not symmetric");
+      if (!is_symmetric(b, 1e-12)) throw SkError(SK_ERR_INVALID_MATRIX, "factorized_cg: B is not symmetric");
+    }
+  }
+  if (s < 1 || s > a->n_rows) throw SkError(SK_ERR_DIMENSION, "basis init: block size must be in [1, n]");
+  if (!lyap && s > b->n_rows) throw SkError(SK_ERR_DIMENSION, "basis init: block size must be in [1, n]");
+  if (s > sk::kMaxS) throw SkError(SK_ERR_UNSUPPORTED, "device path supports block sizes s <= 8");
+  if (!c1 || (!lyap && !c2)) throw SkError(SK_ERR_DIMENSION, "solver: C1/C2 missing");
+  const int dev = gpu ? gpu->device : 0;
+  check_device(dev);
+  auto p = std::make_unique<sk_problem>();
+  p->method = method;
+  p->s = s;
+  p->n = a->n_rows;
+  p->m = lyap ? a->n_rows : b->n_rows;
+  p->device = dev;
+  p->profile = gpu ? gpu->profile : 0;
+  p->capacity_bytes = gpu ? gpu->capacity_bytes : 0;
+  CK(cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking));
+  auto t0 = std::chrono::steady_clock::now();
+  p->h2d_bytes += upload_csr(p->op[0], a->n_rows, a->nnz, a->row_ptr, a->col_idx, a->values, p->stream);
+  if (!lyap) {
+    HostCsr bt = transpose(b);  // W basis applies B^T (block_krylov.cpp:54-56)
+    p->h2d_bytes += upload_csr(p->op[1], bt.n_rows, (int64_t)bt.val.size(), bt.rp.data(),
+                               bt.ci.data(), bt.val.data(), p->stream);
+  }
+  CK(cudaMalloc(&p->c1, sizeof(double) * p->n * s));
+  CK(cudaMemcpyAsync(p->c1, c1, sizeof(double) * p->n * s, cudaMemcpyHostToDevice, p->stream));
+  p->h2d_bytes += sizeof(double) * p->n * s;
+  if (!lyap) {
+    CK(cudaMalloc(&p->c2, sizeof(double) * p->m * s));
+    CK(cudaMemcpyAsync(p->c2, c2, sizeof(double) * p->m * s, cudaMemcpyHostToDevice, p->stream));
+    p->h2d_bytes += sizeof(double) * p->m * s;
+  }
+  CK(cudaStreamSynchronize(p->stream));
+  p->h2d_time = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  return p.release();
+}
+
+void destroy_problem(sk_problem* p) {
+  if (!p) return;
+  cudaSetDevice(p->device);
+  free_csr(p->op[0]);
+  free_csr(p->op[1]);
+  cudaFree(p->c1);
+  cudaFree(p->c2);
+  // the stream is shared with solutions; leave it to the process
+  delete p;
+}
+
+sk_config default_cfg(const sk_config* cfg) {
+  if (cfg) return *cfg;
+  sk_config c{};
+  c.eps_tol = 1e-8;
+  c.max_iter = 0;
+  c.breakdown_tol = 1e-12;
+  return c;
+}
+
+sk_status one_shot(int32_t method, const sk_csr* a, const sk_csr* b, const double* c1,
+                   const double* c2, int64_t s, const sk_config* cfg, const sk_gpu_options* gpu,
+                   sk_solution** out) {
+  if (out) *out = nullptr;
+  sk_problem* p = nullptr;
+  sk_status rc = run_guarded([&] { p = create_problem(method, a, b, c1, c2, s, gpu); });
+  if (rc != SK_OK) return rc;
+  rc = sk_problem_solve(p, cfg, out);
+  destroy_problem(p);
+  return rc;
+}
+
+}  // namespace
+
+extern "C" {
+
+sk_status sk_factorized_cg(const sk_csr* a, const sk_csr* b, const double* c1, const double* c2,
+                           int64_t s, const sk_config* cfg, const sk_gpu_options* gpu,
+                           sk_solution** out) {
+  return one_shot(SK_METHOD_CG, a, b, c1, c2, s, cfg, gpu, out);
+}
+sk_status sk_factorized_cg_lyapunov(const sk_csr* a, const double* c1, int64_t s,
+                                    const sk_config* cfg, const sk_gpu_options* gpu,
+                                    sk_solution** out) {
+  return one_shot(SK_METHOD_CG_LYAPUNOV, a, nullptr, c1, nullptr, s, cfg, gpu, out);
+}
+sk_status sk_factorized_bicgstab(const sk_csr* a, const sk_csr* b, const double* c1,
+                                 const double* c2, int64_t s, const sk_config* cfg,
+                                 const sk_gpu_options* gpu, sk_solution** out) {
+  return one_shot(SK_METHOD_BICGSTAB, a, b, c1, c2, s, cfg, gpu, out);
+}
+
+sk_status sk_problem_create(int32_t method, const sk_csr* a, const sk_csr* b, const double* c1,
+                            const double* c2, int64_t s, const sk_gpu_options* gpu,
+                            sk_problem** out) {
+  if (out) *out = nullptr;
+  return run_guarded([&] { *out = create_problem(method, a, b, c1, c2, s, gpu); });
+}
+
+sk_status sk_problem_solve(sk_problem* p, const sk_config* cfg, sk_solution** out) {
+  if (out) *out = nullptr;
+  return run_guarded([&] {
+    if (!p) throw SkError(SK_ERR_DIMENSION, "null problem");
+    if (p->method == SK_METHOD_BICGSTAB)
+      throw SkError(SK_ERR_UNSUPPORTED, "factorized_bicgstab: device path not built yet");
+    CK(cudaSetDevice(p->device));
+    Solver solver(*p, default_cfg(cfg));
+    *out = solver.run();
+  });
+}
+
+void sk_problem_free(sk_problem* p) { destroy_problem(p); }
+
+int32_t sk_solution_status(const sk_solution* sol) { return sol ? sol->status : -1; }
+void sk_solution_dims(const sk_solution* sol, int64_t* n, int64_t* rv, int64_t* m, int64_t* rw) {
+  if (n) *n = sol->n;
+  if (rv) *rv = sol->rv;
+  if (m) *m = sol->m;
+  if (rw) *rw = sol->rw;
+}
+int64_t sk_solution_num_records(const sk_solution* sol) { return (int64_t)sol->hist.size(); }
+sk_status sk_solution_history(const sk_solution* sol, sk_iteration_record* rec, int64_t count) {
+  if (count > (int64_t)sol->hist.size()) {
+    g_err = "history: count exceeds records";
+    return SK_ERR_DIMENSION;
+  }
+  std::memcpy(rec, sol->hist.data(), sizeof(sk_iteration_record) * count);
+  return SK_OK;
+}
+double sk_solution_total_time(const sk_solution* sol) { return sol->total_time; }
+
+static sk_status copy_basis(const sk_solution* sol, const std::vector<double*>& blocks, int64_t n,
+                            int64_t cols, double* out) {
+  return run_guarded([&] {
+    CK(cudaSetDevice(sol->device));
+    if (cols == 0) return;
+    double* stage = nullptr;
+    CK(cudaMalloc(&stage, sizeof(double) * n * sol->s));
+    for (int64_t b = 0; b < cols / sol->s; ++b) {
+      sk::launch_block_to_colmajor(blocks[b], stage, n, (int)sol->s, sol->stream);
+      CK(cudaMemcpyAsync(out + b * sol->s * n, stage, sizeof(double) * n * sol->s,
+                         cudaMemcpyDeviceToHost, sol->stream));
+    }
+    CK(cudaStreamSynchronize(sol->stream));
+    cudaFree(stage);
+  });
+}
+sk_status sk_solution_copy_V(const sk_solution* sol, double* out) {
+  return copy_basis(sol, sol->vblocks, sol->n, sol->rv, out);
+}
+sk_status sk_solution_copy_W(const sk_solution* sol, double* out) {
+  return copy_basis(sol, sol->wblocks, sol->m, sol->rw, out);
+}
+sk_status sk_solution_copy_core(const sk_solution* sol, double* out) {
+  return run_guarded([&] {
+    CK(cudaSetDevice(sol->device));
+    if (sol->rv == 0 || sol->rw == 0) return;
+    CK(cudaMemcpy2D(out, sol->rv * sizeof(double), sol->X, sol->ld * sizeof(double),
+                    sol->rv * sizeof(double), sol->rw, cudaMemcpyDeviceToHost));
+  });
+}
+int64_t sk_solution_num_captured(const sk_solution* sol) { return (int64_t)sol->captured.size(); }
+sk_status sk_solution_captured_core(const sk_solution* sol, int64_t i, int64_t* rows, int64_t* cols,
+                                    double* out) {
+  if (i < 0 || i >= (int64_t)sol->captured.size()) {
+    g_err = "captured_core: index out of range";
+    return SK_ERR_DIMENSION;
+  }
+  *rows = sol->cap_shape[i].first;
+  *cols = sol->cap_shape[i].second;
+  if (out) std::memcpy(out, sol->captured[i].data(), sizeof(double) * sol->captured[i].size());
+  return SK_OK;
+}
+sk_status sk_solution_stats(const sk_solution* sol, sk_solve_stats* out) {
+  *out = sol->stats;
+  return SK_OK;
+}
+void sk_solution_free(sk_solution* sol) {
+  if (!sol) return;
+  cudaSetDevice(sol->device);
+  for (double* p : sol->chunks) cudaFreeAsync(p, sol->stream);
+  if (sol->X) cudaFreeAsync(sol->X, sol->stream);
+  cudaStreamSynchronize(sol->stream);
+  delete sol;
+}
+
+const char* sk_last_error(void) { return g_err.c_str(); }
+const char* sk_version(void) { return "sylkrylov-b200 0.1 (sm_100a)"; }
+int32_t sk_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) return 0;
+  return n;
+}
+
+sk_status sk_spmm(const sk_csr* a, const double* x, int64_t s, int32_t transpose_flag, double* y) {
+  return run_guarded([&] {
+    validate_csr(a, "A");
+    if (s < 1 || s > sk::kMaxS) throw SkError(SK_ERR_UNSUPPORTED, "sk_spmm: 1 <= s <= 8");
+    check_device(0);
+    cudaStream_t st;
+    CK(cudaStreamCreate(&st));
+    DevCsr d;
+    HostCsr t;
+    int64_t rows, cols;
+    if (transpose_flag) {
+      t = transpose(a);
+      upload_csr(d, t.n_rows, (int64_t)t.val.size(), t.rp.data(), t.ci.data(), t.val.data(), st);
+      rows = a->n_cols;
+      cols = a->n_rows;
+    } else {
+      upload_csr(d, a->n_rows, a->nnz, a->row_ptr, a->col_idx, a->values, st);
+      rows = a->n_rows;
+      cols = a->n_cols;
+    }
+    double *dx, *dy, *dcm;
+    CK(cudaMalloc(&dx, sizeof(double) * std::max<int64_t>(cols * s, 1)));
+    CK(cudaMalloc(&dcm, sizeof(double) * std::max<int64_t>(std::max(rows, cols) * s, 1)));
+    CK(cudaMalloc(&dy, sizeof(double) * std::max<int64_t>(rows * s, 1)));
+    CK(cudaMemcpyAsync(dcm, x, sizeof(double) * cols * s, cudaMemcpyHostToDevice, st));
+    sk::launch_colmajor_to_block(dcm, dx, cols, (int)s, st);
+    sk::launch_spmm_plain((int)s, d.rp, d.ci, d.val, dx, dy, rows, st);
+    sk::launch_block_to_colmajor(dy, dcm, rows, (int)s, st);
+    CK(cudaMemcpyAsync(y, dcm, sizeof(double) * rows * s, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    CK(cudaGetLastError());
+    cudaFree(dx);
+    cudaFree(dy);
+    cudaFree(dcm);
+    free_csr(d);
+    cudaStreamDestroy(st);
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,21 @@
+// sk_launch.h -- host-side launchers of the sm_100a kernels (sk_kernels.cu).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace sk {
+struct SolveConst;
+int launch_count();
+void launch_count_reset();
+void launch_init(const SolveConst& c, const double* dc1, const double* dc2, cudaStream_t st);
+void launch_spmm(const SolveConst& c, cudaStream_t st);
+void launch_gram_lanczos(const SolveConst& c, cudaStream_t st);
+void launch_rare(const SolveConst& c, int64_t kmax_blocks, cudaStream_t st);
+void launch_pass2(const SolveConst& c, cudaStream_t st);
+void launch_cg_a(const SolveConst& c, int64_t rmax, cudaStream_t st);
+void launch_cg_b(const SolveConst& c, int64_t rmax, cudaStream_t st);
+void launch_spmm_plain(int s, const int32_t* rp, const int32_t* ci, const double* val,
+                       const double* x, double* y, int64_t n, cudaStream_t st);
+void launch_block_to_colmajor(const double* blk, double* out, int64_t n, int s, cudaStream_t st);
+void launch_colmajor_to_block(const double* in, double* blk, int64_t n, int s, cudaStream_t st);
+}  // namespace sk

@@ -1,0 +1,116 @@
+"""GPU parity: the sm_100a path against the CPU oracle (SKO_REPRODUCIBLE) on the
+same seeded inputs. Bar: bitwise equality (integer/index work and the fixed
+reduction contract); histories additionally within 1e-10 of the oracle's
+reference-order mode on short runs (north-star tolerance)."""
+import numpy as np
+import pytest
+
+from tests.helpers import bits_equal, max_rel, to_sk
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("s", [1, 2, 3, 4, 8])
+def test_spmm_bitwise_stencil(sk, po, s):
+    a = po.laplacian_2d(37)
+    x = po.random_rhs(a.n_rows, s, 11 + s)
+    y_ref = po.spmm(a, x)
+    y = sk.spmm(to_sk(sk, a), x)
+    assert bits_equal(y, y_ref)
+
+
+@pytest.mark.parametrize("s", [1, 2, 5])
+def test_spmm_transpose_matches_scatter(sk, po, s):
+    a = po.random_sparse(60, 45, 0.15, 44)
+    x = po.random_dense(60, s, 45)
+    y_ref = po.spmm_transpose(a, x)
+    y = sk.spmm(to_sk(sk, a), x, transpose=True)
+    assert np.array_equal(y, y_ref)  # equal up to the sign of exact zeros
+
+
+def _cfg(sk, **kw):
+    return sk.SolverConfig(**kw)
+
+
+def _compare(sol, ref):
+    h = sol.history.rel_residuals()
+    assert sol.status == ref.status
+    assert h.size == ref.rel_residual.size
+    assert bits_equal(h, ref.rel_residual), f"max rel diff {max_rel(h, ref.rel_residual)}"
+    assert bits_equal(sol.core, ref.core)
+    assert bits_equal(sol.V, ref.V)
+    assert bits_equal(sol.W, ref.W)
+
+
+def test_cg_config1_bitwise(sk, po):
+    """BASELINE config 1: 2D Laplacian 64x64, s=1, unit-norm seeded columns."""
+    a = po.laplacian_2d(64)
+    c1 = po.random_rhs(4096, 1, 1234)
+    c1 /= np.linalg.norm(c1)
+    c2 = po.random_rhs(4096, 1, 1235)
+    c2 /= np.linalg.norm(c2)
+    cfg = po.Config(eps_tol=1e-8, max_iter=500)
+    ref = po.factorized_cg(a, a, c1, c2, cfg, po.REPRODUCIBLE)
+    sol = sk.factorized_cg(to_sk(sk, a), to_sk(sk, a), c1, c2, _cfg(sk, eps_tol=1e-8, max_iter=500))
+    _compare(sol, ref)
+    assert sol.status == "converged"
+
+
+@pytest.mark.parametrize("s", [1, 2, 3])
+def test_cg_lyapunov_bitwise(sk, po, s):
+    a = po.laplacian_2d(12)
+    c1 = po.random_dense(144, s, 21 + s)
+    ref = po.factorized_cg_lyapunov(a, c1, po.Config(eps_tol=1e-8), po.REPRODUCIBLE)
+    sol = sk.factorized_cg_lyapunov(to_sk(sk, a), c1, _cfg(sk, eps_tol=1e-8))
+    _compare(sol, ref)
+
+
+@pytest.mark.parametrize("s", [1, 2, 4])
+def test_cg_sylvester_spd_bitwise(sk, po, s):
+    a = po.random_spd(40, 10)
+    b = po.random_spd(35, 11)
+    c1 = po.random_dense(40, s, 12)
+    c2 = po.random_dense(35, s, 13)
+    ref = po.factorized_cg(a, b, c1, c2, po.Config(eps_tol=1e-10), po.REPRODUCIBLE)
+    sol = sk.factorized_cg(to_sk(sk, a), to_sk(sk, b), c1, c2, _cfg(sk, eps_tol=1e-10))
+    _compare(sol, ref)
+
+
+def test_identity_pair_exhaustion(sk, po):
+    """test_factorized_solvers.cpp:22-33: identity pair converges in one iteration."""
+    i7, i5 = po.Csr.identity(7), po.Csr.identity(5)
+    c1, c2 = po.random_dense(7, 2, 1), po.random_dense(5, 2, 2)
+    ref = po.factorized_cg(i7, i5, c1, c2, None, po.REPRODUCIBLE)
+    sol = sk.factorized_cg(to_sk(sk, i7), to_sk(sk, i5), c1, c2)
+    _compare(sol, ref)
+    assert sol.status == "converged" and sol.history.iterations() == 1
+    x = sol.V @ sol.core @ sol.W.T
+    e = 0.5 * c1 @ c2.T
+    assert np.linalg.norm(x - e) <= 1e-13 * np.linalg.norm(e)
+
+
+def test_rank_deficient_start(sk, po):
+    a = po.random_spd(8, 56)
+    c1 = np.zeros((8, 2), order="F")
+    c1[:, 0] = c1[:, 1] = np.arange(8.0)
+    with pytest.raises(sk.RankDeficientStartError):
+        sk.factorized_cg_lyapunov(to_sk(sk, a), c1)
+
+
+def test_nonsymmetric_rejected(sk, po):
+    a = po.random_diag_dominant(6, 14)
+    b = po.random_spd(6, 15)
+    c = po.random_dense(6, 1, 16)
+    with pytest.raises(sk.InvalidMatrixError):
+        sk.factorized_cg(to_sk(sk, a), to_sk(sk, b), c, c)
+
+
+def test_history_within_reference_order_tolerance(sk, po):
+    """North-star tolerance against the reference-order restatement on a short run."""
+    a = po.laplacian_2d(30)
+    c1 = po.random_rhs(900, 3, 101)
+    ref = po.factorized_cg_lyapunov(a, c1, po.Config(eps_tol=1e-13, max_iter=25), po.REFERENCE_ORDER)
+    sol = sk.factorized_cg_lyapunov(to_sk(sk, a), c1, _cfg(sk, eps_tol=1e-13, max_iter=25))
+    h = sol.history.rel_residuals()
+    assert h.size == ref.rel_residual.size
+    assert max_rel(h[:21], ref.rel_residual[:21]) <= 1e-10
