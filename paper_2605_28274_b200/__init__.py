@@ -241,7 +241,7 @@ class FactorizedSolution:
             "classes": {KERNEL_CLASSES[i]: {"time_s": st.class_time_s[i],
                                              "launches": st.class_launches[i],
                                              "bytes": st.class_bytes[i]} for i in range(9)},
-            "paths": dict(zip(["pythagorean", "explicit", "householder", "cleanup"], list(st.paths))),
+            "paths": dict(zip(["direct", "householder", "cleanup", "unused"], list(st.paths))),
         }
         self.captured_cores = []
         for i in range(int(L.sk_solution_num_captured(handle))):

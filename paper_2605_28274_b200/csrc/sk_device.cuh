@@ -29,27 +29,26 @@ enum Status : int { RUNNING = 0, CONVERGED = 1, MAXITER = 2, BREAKDOWN = 3, RANK
 // per-extension stage machine of one basis side
 enum Stage : int {
   ST_NONE = 0,
-  ST_GROW_PYTH,         // normal: V_k = (base - sum V_b cc_b) R^-1 on the fly
-  ST_GROW_WX,           // V_k = wx R^-1 (wx materialised)
-  ST_GROW_HH,           // V_k = Householder Q (in qh)
-  ST_NEED_MAT,          // Pythagorean Gram rejected: materialise wx + direct Gram
-  ST_NEED_MAT_CLEANUP,  // Pythagorean ok but Lanczos clean-up requested
-  ST_NEED_HH,           // direct Gram ambiguous: Householder on wx
-  ST_NEED_CLEANUP,      // Lanczos clean-up: Gram vs all blocks, update, direct Gram
-  ST_NEED_HH2,          // Householder after clean-up
-  ST_DONE_NOGROW        // exhausted or broken this step (no new block)
+  ST_GROW_DIRECT,   // accepted: U_k holds the candidate, N_k = R (CholQR of the direct Gram)
+  ST_GROW_HH,       // accepted: U_k holds the Householder Q, N_k = I
+  ST_NEED_HH,       // direct Gram ambiguous: Householder on the candidate (first pass)
+  ST_NEED_CLEANUP,  // Lanczos clean-up: Gram vs all blocks, update, direct Gram
+  ST_NEED_HH2,      // Householder after the clean-up
+  ST_DONE_NOGROW,   // exhausted or broken this step (no new block)
+  ST_INIT_DIRECT,   // init: U_0 = C, N_0 = R
+  ST_INIT_HH        // init: U_0 = Householder Q of C, N_0 = I
 };
 
 struct SideState {
   int64_t blocks;      // orthonormal blocks in V
   int64_t steps;       // completed extensions (H block columns)
-  int32_t exhausted, broken, stage, cleanup_done;
+  int32_t exhausted, broken, stage, pad;
   double hfro2;        // running ||H||_F^2
   double coeff2, r2, scale;
   double smax, smin;
   double R[kMaxS * kMaxS];      // triangular factor of the current candidate
-  double gbase[kMaxS * kMaxS];  // R1 Gram of the base candidate
-  int64_t paths[4];             // pythagorean / explicit / householder / cleanup
+  double gbase[kMaxS * kMaxS];  // R1 Gram of the candidate
+  int64_t paths[4];             // direct / householder / clean-up / unused
 };
 
 struct DevState {
@@ -73,11 +72,12 @@ struct SideConst {
   const double* val;
   double* const* blocks;     // device table of block pointers (row-interleaved n x s)
   double* w;                 // scratch n x s: op * V_last
-  double* wx;                // scratch n x s: materialised candidate / CGS2 base
+  double* wx;                // scratch n x s: CGS2 intermediate / transposed start block
   double* qh;                // scratch n x s: Householder Q
   double* hw;                // scratch n x s: Householder work copy
   double* hband;             // Lanczos H bands [cap_steps][3][s*s] | Arnoldi dense H
   int64_t hld;               // Arnoldi: leading dimension of the dense H
+  double* nfac;              // [cap_blocks][s*s + s] normalisation factor N_b and 1/diag
   double* coef;              // [cap_blocks][s*s] CGS coefficients (pass 1)
   double* coef2;             // [cap_blocks][s*s] second-pass coefficients
   double* part;              // R1 CTA partials

@@ -10,6 +10,8 @@
 #include "sk_launch.h"
 
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <chrono>
 #include <cmath>
 #include <cstring>
@@ -174,7 +176,9 @@ struct sk_solution {
   std::vector<std::pair<int64_t, int64_t>> cap_shape;
   double total_time = 0.0;
   sk_solve_stats stats{};
-  std::vector<double*> vblocks, wblocks;  // block pointers (row-interleaved n x s)
+  std::vector<double*> vblocks, wblocks;  // block pointers (row-interleaved n x s, unnormalised)
+  double* vnfac = nullptr;                // per-block normalisation factors (owned)
+  double* wnfac = nullptr;
   std::vector<double*> chunks;            // owned allocations
   double* X = nullptr;                    // owned core buffer
   int64_t ld = 0;
@@ -191,7 +195,7 @@ int64_t resolve_max_iter(const sk_config& c, int64_t n, int64_t m) {
 struct SideBuf {
   int64_t n = 0;
   double *w = nullptr, *wx = nullptr, *qh = nullptr, *hw = nullptr;
-  double *hband = nullptr, *coef = nullptr, *coef2 = nullptr, *part = nullptr;
+  double *hband = nullptr, *coef = nullptr, *coef2 = nullptr, *part = nullptr, *nfac = nullptr;
   unsigned int* counter = nullptr;
   double** table = nullptr;
   double** table_host = nullptr;  // pinned mirror (async uploads)
@@ -225,7 +229,22 @@ struct Solver {
   std::vector<cudaEvent_t> pool;
   sk_solve_stats stats{};
 
-  explicit Solver(sk_problem& p, const sk_config& cf) : P(p), cfg(cf), st(p.stream) {}
+  explicit Solver(sk_problem& p, const sk_config& cf) : P(p), cfg(cf), st(p.stream) {
+    const char* e = getenv("SK_DEBUG_SYNC");
+    debug_sync = e && e[0] == '1';
+  }
+  bool debug_sync = false;
+  void dbg(const char* what, int64_t k) {
+    if (!debug_sync) return;
+    cudaError_t e = cudaStreamSynchronize(st);
+    if (e == cudaSuccess) e = cudaGetLastError();
+    sk::DevState hs;
+    cudaMemcpy(&hs, dstate, sizeof hs, cudaMemcpyDeviceToHost);
+    fprintf(stderr, "[sk] k=%lld %-14s err=%s status=%d blocks=%lld/%lld stage=%d/%d\n", (long long)k,
+            what, cudaGetErrorString(e), hs.status, (long long)hs.side[0].blocks,
+            (long long)hs.side[1].blocks, hs.side[0].stage, hs.side[1].stage);
+    if (e != cudaSuccess) throw SkError(SK_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+  }
 
   template <class T>
   T* dalloc(size_t count, bool zero = true) {
@@ -309,6 +328,7 @@ struct Solver {
         b.hband = dalloc<double>((cap_blocks + 1) * 3 * s * s);
       }
       b.coef = dalloc<double>(cap_blocks * s * s);
+      b.nfac = dalloc<double>(cap_blocks * (s * s + s));
       b.coef2 = dalloc<double>(cap_blocks * s * s);
       b.part = dalloc<double>(std::max<int64_t>((cap_blocks + 3) * ncta * s * s, nseg + 64));
       b.counter = dalloc<unsigned int>(cap_blocks + 8);
@@ -327,6 +347,7 @@ struct Solver {
       sc.hband = b.hband;
       sc.hld = b.hld;
       sc.coef = b.coef;
+      sc.nfac = b.nfac;
       sc.coef2 = b.coef2;
       sc.part = b.part;
       sc.counter = b.counter;
@@ -421,6 +442,7 @@ struct Solver {
     for (int sd = 0; sd < nsides; ++sd) ensure_blocks(sd, 1);
     CK(cudaEventRecord(t0, st));
     sk::launch_init(c, P.c1, lyap ? P.c1 : P.c2, st);
+    dbg("init", -1);
     int32_t status = 0;
     CK(cudaMemcpyAsync(&status, &dstate->status, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
@@ -444,11 +466,17 @@ struct Solver {
       grow_cores((k + 2) * s);
       const double rp = (double)((k + 1) * s), rq = (double)((k + 2) * s);
       timed(0, spmm_bytes(), [&] { sk::launch_spmm(c, st); });
-      timed(1, pass_bytes(k, 1), [&] { sk::launch_gram_lanczos(c, st); });
+      dbg("spmm", k);
+      timed(1, pass_bytes(k, 1), [&] { sk::launch_lanczos_gram(c, st); });
+      dbg("gram", k);
+      timed(3, pass_bytes(k, 2), [&] { sk::launch_lanczos_update(c, k + 1, st); });
+      dbg("update", k);
       timed(2, 0.0, [&] { sk::launch_rare(c, k + 1, st); });
-      timed(3, pass_bytes(k, 2), [&] { sk::launch_pass2(c, st); });
+      dbg("rare", k);
       timed(4, 8.0 * 3 * rp * rp, [&] { sk::launch_cg_a(c, (k + 1) * s, st); });
+      dbg("core_a", k);
       timed(5, 8.0 * (4 * rp * rp + rq * rq), [&] { sk::launch_cg_b(c, (k + 2) * s, st); });
+      dbg("core_b", k);
       CK(cudaMemcpyAsync(&hstat[k % RING], &dstate->status, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
       CK(cudaEventRecord(rev[k % RING], st));
       enq = k + 1;
@@ -577,6 +605,9 @@ struct Solver {
     dfree(hist_tb);
     dfree(dstate);
     if (sol) {
+      sol->vnfac = side[0].nfac;
+      sol->wnfac = side[nsides > 1 ? 1 : 0].nfac;
+      if (nsides > 1 && side[1].nfac == side[0].nfac) sol->wnfac = sol->vnfac;
       sol->chunks = chunks;
       sol->X = X;
       sol->ld = rcap;
@@ -587,6 +618,7 @@ struct Solver {
     } else {
       for (double* p : chunks) dfree(p);
       dfree(X);
+      for (int sd = 0; sd < nsides; ++sd) dfree(side[sd].nfac);
     }
     cudaStreamSynchronize(st);
   }
@@ -760,15 +792,15 @@ sk_status sk_solution_history(const sk_solution* sol, sk_iteration_record* rec, 
 }
 double sk_solution_total_time(const sk_solution* sol) { return sol->total_time; }
 
-static sk_status copy_basis(const sk_solution* sol, const std::vector<double*>& blocks, int64_t n,
-                            int64_t cols, double* out) {
+static sk_status copy_basis(const sk_solution* sol, const std::vector<double*>& blocks,
+                            const double* nfac, int64_t n, int64_t cols, double* out) {
   return run_guarded([&] {
     CK(cudaSetDevice(sol->device));
     if (cols == 0) return;
     double* stage = nullptr;
     CK(cudaMalloc(&stage, sizeof(double) * n * sol->s));
     for (int64_t b = 0; b < cols / sol->s; ++b) {
-      sk::launch_block_to_colmajor(blocks[b], stage, n, (int)sol->s, sol->stream);
+      sk::launch_export_block((int)sol->s, blocks[b], nfac, b, stage, n, sol->stream);
       CK(cudaMemcpyAsync(out + b * sol->s * n, stage, sizeof(double) * n * sol->s,
                          cudaMemcpyDeviceToHost, sol->stream));
     }
@@ -777,10 +809,10 @@ static sk_status copy_basis(const sk_solution* sol, const std::vector<double*>& 
   });
 }
 sk_status sk_solution_copy_V(const sk_solution* sol, double* out) {
-  return copy_basis(sol, sol->vblocks, sol->n, sol->rv, out);
+  return copy_basis(sol, sol->vblocks, sol->vnfac, sol->n, sol->rv, out);
 }
 sk_status sk_solution_copy_W(const sk_solution* sol, double* out) {
-  return copy_basis(sol, sol->wblocks, sol->m, sol->rw, out);
+  return copy_basis(sol, sol->wblocks, sol->wnfac, sol->m, sol->rw, out);
 }
 sk_status sk_solution_copy_core(const sk_solution* sol, double* out) {
   return run_guarded([&] {
@@ -811,6 +843,8 @@ void sk_solution_free(sk_solution* sol) {
   cudaSetDevice(sol->device);
   for (double* p : sol->chunks) cudaFreeAsync(p, sol->stream);
   if (sol->X) cudaFreeAsync(sol->X, sol->stream);
+  if (sol->vnfac) cudaFreeAsync(sol->vnfac, sol->stream);
+  if (sol->wnfac && sol->wnfac != sol->vnfac) cudaFreeAsync(sol->wnfac, sol->stream);
   cudaStreamSynchronize(sol->stream);
   delete sol;
 }

@@ -1,21 +1,26 @@
 // sk_kernels.cu -- sm_100a kernels of the factorized-Krylov hot path.
 //
-//  K1  k_spmm<S>          w = op * V_last (CSR gather, stored order, mul+add)
-//  K2  k_gram<S>          R1 Gram coefficients V_b^T x (+ x^T x) with last-CTA trees
-//      k_update<S>        x -= sum_b V_b c_b (+ R1 self Gram)
-//  K3  k_pass2<S>         V_k = (base - V cc) R^-1 (forward substitution per row)
-//      k_householder      rare-path single-CTA Householder QR (exact classification)
-//  K4  k_cg_a<S>/k_cg_b<S> fused CG core updates: P = R + beta P, Q = H P + P G^T on
-//                         the fly from the Lanczos bands, <R,Q>, X += alpha P,
-//                         R -= alpha Q, ||R||^2 (R2 tile trees)
+// Basis blocks are stored UNNORMALISED (U_b, row-interleaved n x s) together
+// with their triangular factor N_b and 1/diag(N_b); every reader forms the
+// orthonormal row v_b(i,:) = U_b(i,:) N_b^{-1} on the fly (forward substitution
+// with the reciprocal diagonal). The candidate of each extension is written
+// straight into the next block's storage, so an extension needs no separate
+// normalisation pass:
+//
+//  K1  k_spmm<S>       w = op * V_last (CSR gather in stored order, mul+add)
+//  K2  k_gram<S>       R1 Gram coefficients V_b^T x, last-CTA trees (fixed order)
+//      k_update<S>     x_out = x_in - sum_b V_b c_b, + R1 Gram of x_out, finalise
+//                      (Cholesky, sigma extremes, classification, H column)
+//      k_householder   rare path: single-CTA Householder QR (exact classification)
+//  K4  k_cg_a/k_cg_b   fused CG core updates (P = R + beta P; Q = H P + P G^T on the
+//                      fly from the Lanczos bands; <R,Q>; X += alpha P; R -= alpha Q;
+//                      ||R||^2) with R2 tile trees
 //
 // Reference ops restated (proj/src): sparse_matrix.cpp:142-200 (SpMM),
-// block_krylov.cpp:63-145 (extension), :173-213 (banded products),
-// factorized_solvers.cpp:134-192 (CG loop), decompositions.cpp:16-78 (QR).
+// block_krylov.cpp:27-145 (init / extension), :173-213 (banded products),
+// factorized_solvers.cpp:121-192 (CG loop), decompositions.cpp:16-78 (QR).
 #include "sk_device.cuh"
 #include "sk_launch.h"
-
-#include <cstdio>
 
 namespace sk {
 
@@ -26,37 +31,74 @@ __device__ __forceinline__ uint64_t globaltimer() {
 }
 
 // =====================================================================
-// Side finalisation logic (single thread). Mirrors oracle norm_repro +
-// classification (block_krylov.cpp:102-144).
+// On-the-fly normalisation of basis rows
 // =====================================================================
-struct FinalCtx {
-  const SolveConst* c;
-  int side;
+template <int S>
+struct NF {
+  double N[S * S];
+  double d[S];
 };
-
-__device__ inline double* hb_ptr(const SideConst& sc, int64_t e, int d, int s) {
-  return sc.hband + (e * 3 + d) * (int64_t)(s * s);
+template <int S>
+__device__ __forceinline__ void load_nf(const double* nfac, int64_t b, NF<S>& f) {
+  const double* p = nfac + b * (S * S + S);
+#pragma unroll
+  for (int e = 0; e < S * S; ++e) f.N[e] = __ldg(p + e);
+#pragma unroll
+  for (int u = 0; u < S; ++u) f.d[u] = __ldg(p + S * S + u);
+}
+template <int S>
+__device__ __forceinline__ void norm_row(const double* u, const NF<S>& f, double* q) {
+#pragma unroll
+  for (int c = 0; c < S; ++c) {
+    double acc = u[c];
+#pragma unroll
+    for (int t = 0; t < c; ++t) acc = __dsub_rn(acc, __dmul_rn(q[t], f.N[c * S + t]));
+    q[c] = __dmul_rn(acc, f.d[c]);
+  }
+}
+template <int S>
+__device__ __forceinline__ void load_vrow(const double* blk, const NF<S>& f, int64_t i, double* q) {
+  double u[S];
+#pragma unroll
+  for (int t = 0; t < S; ++t) u[t] = __ldg(blk + i * S + t);
+  norm_row<S>(u, f, q);
 }
 
-// first block of the orthogonalisation window J
+// =====================================================================
+// Single-thread finalisation logic (mirrors oracle sk_basis_try_extend)
+// =====================================================================
 __device__ inline int64_t first_block(const SolveConst& c, int64_t k) {
   return c.arnoldi ? 0 : (k - 2 > 0 ? k - 2 : 0);
 }
+__device__ inline double* hb_ptr(const SideConst& sc, int64_t e, int d, int s) {
+  return sc.hband + (e * 3 + d) * (int64_t)(s * s);
+}
+__device__ inline double* hcol_ptr(const SideConst& sc, int64_t e, int cc, int s) {
+  return sc.hband + (e * s + cc) * sc.hld;
+}
 
-// coeff2 in the reference loop order (block_krylov.cpp:105-108) over J blocks
-__device__ inline double coeff2_of(const SolveConst& c, const SideConst& sc, int64_t k) {
+// coeff2 in the reference loop order (block_krylov.cpp:105-108)
+__device__ inline double coeff2_of(const SolveConst& c, int side, int64_t k, int64_t e) {
+  const SideConst& sc = c.side[side];
   const int s = c.s, ss = s * s;
   double acc = 0.0;
-  for (int64_t jb = first_block(c, k); jb < k; ++jb) {
-    const double* h = sc.coef + jb * ss;
+  for (int64_t jb = first_block(c, k); jb < k; ++jb)
     for (int cc = 0; cc < s; ++cc)
-      for (int r = 0; r < s; ++r) acc = __dadd_rn(acc, __dmul_rn(h[cc * s + r], h[cc * s + r]));
-  }
+      for (int r = 0; r < s; ++r) {
+        const double h = c.arnoldi ? __ldcg(hcol_ptr(sc, e, cc, s) + jb * s + r)
+                                   : __ldcg(sc.coef + jb * ss + cc * s + r);
+        acc = __dadd_rn(acc, __dmul_rn(h, h));
+      }
   return acc;
 }
 
-// Commit the outcome of an extension step into H / counters.
-__device__ inline void commit_grow(const SolveConst& c, int side) {
+__device__ inline void set_nfac(const SideConst& sc, int64_t b, int s, const double* N, bool identity) {
+  double* p = sc.nfac + b * (s * s + s);
+  for (int e = 0; e < s * s; ++e) p[e] = identity ? ((e % (s + 1)) == 0 ? 1.0 : 0.0) : N[e];
+  for (int u = 0; u < s; ++u) p[s * s + u] = __ddiv_rn(1.0, p[u * s + u]);
+}
+
+__device__ inline void commit_grow(const SolveConst& c, int side, int grow_stage) {
   const SideConst& sc = c.side[side];
   SideState& st = c.st->side[side];
   const int s = c.s, ss = s * s;
@@ -66,22 +108,19 @@ __device__ inline void commit_grow(const SolveConst& c, int side) {
     double* h1 = hb_ptr(sc, e, 1, s);
     double* h2 = hb_ptr(sc, e, 2, s);
     for (int x = 0; x < ss; ++x) {
-      h0[x] = (k >= 2) ? sc.coef[(k - 2) * ss + x] : 0.0;
-      h1[x] = sc.coef[(k - 1) * ss + x];
+      h0[x] = (k >= 2) ? __ldcg(sc.coef + (k - 2) * ss + x) : 0.0;
+      h1[x] = __ldcg(sc.coef + (k - 1) * ss + x);
       h2[x] = st.R[x];
     }
   } else {
-    // dense upper block Hessenberg column e: rows [0, (k+1)s)
-    for (int cc = 0; cc < s; ++cc) {
-      double* col = sc.hband + (e * s + cc) * sc.hld;
-      for (int64_t jb = 0; jb < k; ++jb)
-        for (int r = 0; r < s; ++r) col[jb * s + r] = sc.coef[jb * ss + cc * s + r];
-      for (int r = 0; r < s; ++r) col[k * s + r] = st.R[cc * s + r];
-    }
+    for (int cc = 0; cc < s; ++cc)
+      for (int r = 0; r < s; ++r) hcol_ptr(sc, e, cc, s)[k * s + r] = st.R[cc * s + r];
   }
+  set_nfac(sc, k, s, st.R, grow_stage == ST_GROW_HH);
   st.hfro2 = __dadd_rn(__dadd_rn(st.hfro2, st.coeff2), st.r2);
   st.steps = e + 1;
   st.blocks = k + 1;
+  st.stage = grow_stage;
 }
 __device__ inline void commit_exhausted(const SolveConst& c, int side) {
   const SideConst& sc = c.side[side];
@@ -93,17 +132,13 @@ __device__ inline void commit_exhausted(const SolveConst& c, int side) {
     double* h1 = hb_ptr(sc, e, 1, s);
     double* h2 = hb_ptr(sc, e, 2, s);
     for (int x = 0; x < ss; ++x) {
-      h0[x] = (k >= 2) ? sc.coef[(k - 2) * ss + x] : 0.0;
-      h1[x] = sc.coef[(k - 1) * ss + x];
+      h0[x] = (k >= 2) ? __ldcg(sc.coef + (k - 2) * ss + x) : 0.0;
+      h1[x] = __ldcg(sc.coef + (k - 1) * ss + x);
       h2[x] = 0.0;
     }
   } else {
-    for (int cc = 0; cc < s; ++cc) {
-      double* col = sc.hband + (e * s + cc) * sc.hld;
-      for (int64_t jb = 0; jb < k; ++jb)
-        for (int r = 0; r < s; ++r) col[jb * s + r] = sc.coef[jb * ss + cc * s + r];
-      for (int r = 0; r < s; ++r) col[k * s + r] = 0.0;
-    }
+    for (int cc = 0; cc < s; ++cc)
+      for (int r = 0; r < s; ++r) hcol_ptr(sc, e, cc, s)[k * s + r] = 0.0;
   }
   st.hfro2 = __dadd_rn(st.hfro2, st.coeff2);
   st.steps = e + 1;
@@ -111,19 +146,18 @@ __device__ inline void commit_exhausted(const SolveConst& c, int side) {
   st.stage = ST_DONE_NOGROW;
 }
 
-// Classification after sigma extremes are known. first_pass: compute scale.
-// grow_stage: stage to use when the block is accepted.
+// classification (block_krylov.cpp:105-137)
 __device__ inline void classify(const SolveConst& c, int side, bool first_pass, int grow_stage) {
   SideState& st = c.st->side[side];
   const int s = c.s, ss = s * s;
   if (first_pass) {
-    st.coeff2 = coeff2_of(c, c.side[side], st.blocks);
+    st.coeff2 = coeff2_of(c, side, st.blocks, st.steps);
     double r2 = 0.0;
     for (int x = 0; x < ss; ++x) r2 = __dadd_rn(r2, __dmul_rn(st.R[x], st.R[x]));
     st.r2 = r2;
     st.scale = __dsqrt_rn(__dadd_rn(__dadd_rn(st.hfro2, st.coeff2), st.r2));
     if (!c.arnoldi && st.smin < __dmul_rn(c.tol, st.scale)) {
-      st.stage = (grow_stage == ST_GROW_PYTH) ? ST_NEED_MAT_CLEANUP : ST_NEED_CLEANUP;
+      st.stage = ST_NEED_CLEANUP;
       return;
     }
   }
@@ -137,45 +171,10 @@ __device__ inline void classify(const SolveConst& c, int side, bool first_pass, 
     st.stage = ST_DONE_NOGROW;
     return;
   }
-  st.stage = grow_stage;
-  commit_grow(c, side);
+  commit_grow(c, side, grow_stage);
 }
 
-// After the Pythagorean Gram is known (gbase, coefficients cc over blocks [c0,k)).
-__device__ inline void finalize_pyth(const SolveConst& c, int side, const double* cc, int64_t c0,
-                                     int64_t c1) {
-  SideState& st = c.st->side[side];
-  const int s = c.s, ss = s * s;
-  double G[kMaxS * kMaxS];
-  for (int u = 0; u < s; ++u)
-    for (int t = 0; t < s; ++t) {
-      double acc = st.gbase[u * s + t];
-      for (int64_t b = c0; b < c1; ++b) {
-        const double* cb = cc + b * ss;
-        for (int v = 0; v < s; ++v) acc = __dsub_rn(acc, __dmul_rn(cb[t * s + v], cb[u * s + v]));
-      }
-      G[u * s + t] = acc;
-    }
-  bool ok = true;
-  for (int u = 0; u < s; ++u)
-    if (!(G[u * s + u] > __dmul_rn(st.gbase[u * s + u], kPythGuard))) ok = false;
-  if (ok) ok = cholesky_upper(G, s, st.R);
-  if (ok) {
-    jacobi_extremes(st.R, s, s, &st.smax, &st.smin);
-    if (st.smin < __dmul_rn(kHHRatio, st.smax)) {
-      st.stage = ST_NEED_MAT;  // materialise, then Householder (no direct Gram)
-      st.cleanup_done = 2;     // marker: skip direct Gram
-      return;
-    }
-    st.paths[0]++;
-    classify(c, side, true, ST_GROW_PYTH);
-    return;
-  }
-  st.stage = ST_NEED_MAT;
-  st.cleanup_done = 0;
-}
-
-// After a direct Gram of the materialised wx (gbase holds it).
+// after the direct Gram (gbase) of the candidate in U_k
 __device__ inline void finalize_direct(const SolveConst& c, int side, bool first_pass) {
   SideState& st = c.st->side[side];
   const int s = c.s;
@@ -188,21 +187,35 @@ __device__ inline void finalize_direct(const SolveConst& c, int side, bool first
     st.stage = first_pass ? ST_NEED_HH : ST_NEED_HH2;
     return;
   }
-  if (first_pass) st.paths[1]++;
-  classify(c, side, first_pass, ST_GROW_WX);
+  if (first_pass) st.paths[0]++;
+  classify(c, side, first_pass, ST_GROW_DIRECT);
+}
+__device__ inline void finalize_init(const SolveConst& c, int side) {
+  SideState& st = c.st->side[side];
+  const int s = c.s;
+  bool ok = cholesky_upper(st.gbase, s, st.R);
+  if (ok) {
+    jacobi_extremes(st.R, s, s, &st.smax, &st.smin);
+    if (st.smin < __dmul_rn(kHHRatio, st.smax)) ok = false;
+  }
+  if (ok) {
+    set_nfac(c.side[side], 0, s, st.R, false);
+    st.stage = ST_INIT_DIRECT;
+    st.paths[0]++;
+  } else {
+    st.stage = ST_INIT_HH;
+    st.paths[1]++;
+  }
 }
 
 // =====================================================================
 // R1 machinery: per-CTA aligned subtree over 32 segments
 // =====================================================================
-// Lane-owner storage of NE entries after butterflies: lane owns e = lane + 32*j.
 template <int NE>
 struct OwnerVals {
   static constexpr int J = (NE + 31) / 32;
   double v[J > 0 ? J : 1];
 };
-
-// Combine the per-lane accumulators of one segment into owner registers.
 template <int NE>
 __device__ __forceinline__ void seg_butterfly(const double* acc, OwnerVals<NE>& out, int lane) {
 #pragma unroll
@@ -211,9 +224,6 @@ __device__ __forceinline__ void seg_butterfly(const double* acc, OwnerVals<NE>& 
     if ((e & 31) == lane) out.v[e >> 5] = v;
   }
 }
-
-// After the warp's 4 segments produced owner values segv[q], build the warp node
-// and then the CTA node; thread e < NE writes part_out[e].
 template <int NE>
 __device__ __forceinline__ void cta_combine(OwnerVals<NE> (&segv)[kSegsPerWarp], int nvalid_warp,
                                             int nvalid_cta_segs, double* part_out) {
@@ -237,6 +247,27 @@ __device__ __forceinline__ void cta_combine(OwnerVals<NE> (&segv)[kSegsPerWarp],
     part_out[e] = tree_reduce_local(a, nwarps);
   }
 }
+struct SegGeom {
+  int64_t seg_w0;
+  int nvalid_cta, nvalid_warp;
+};
+__device__ __forceinline__ SegGeom seg_geom(int64_t cta, int64_t nseg) {
+  SegGeom g;
+  const int warp = threadIdx.x >> 5;
+  const int64_t seg_cta0 = cta * kSegsPerCta;
+  g.nvalid_cta = (int)mn64(kSegsPerCta, nseg - seg_cta0);
+  g.seg_w0 = seg_cta0 + warp * kSegsPerWarp;
+  g.nvalid_warp = (int)mx64(0, mn64(kSegsPerWarp, nseg - g.seg_w0));
+  return g;
+}
+__device__ __forceinline__ void unpack_tri(int e, int& t, int& u) {
+  u = 0;
+  t = e;
+  while (t > u) {
+    t -= u + 1;
+    ++u;
+  }
+}
 
 // =====================================================================
 // K1: SpMM  w = op * V_last   (sparse_matrix.cpp:142-158, order preserved)
@@ -250,7 +281,10 @@ __global__ void __launch_bounds__(256) k_spmm(SolveConst c) {
   const SideState& ss = st->side[side];
   if (ss.exhausted || ss.broken) return;
   const SideConst& sc = c.side[side];
-  const double* __restrict__ x = sc.blocks[ss.blocks - 1];
+  const int64_t kl = ss.blocks - 1;
+  const double* __restrict__ x = sc.blocks[kl];
+  NF<S> f;
+  load_nf<S>(sc.nfac, kl, f);
   double* __restrict__ w = sc.w;
   const int64_t n = sc.n;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
@@ -262,8 +296,10 @@ __global__ void __launch_bounds__(256) k_spmm(SolveConst c) {
     for (int32_t kk = k0; kk < k1; ++kk) {
       const int64_t col = __ldg(sc.ci + kk);
       const double v = __ldg(sc.val + kk);
+      double q[S];
+      load_vrow<S>(x, f, col, q);
 #pragma unroll
-      for (int u = 0; u < S; ++u) acc[u] = __dadd_rn(acc[u], __dmul_rn(v, __ldg(x + col * S + u)));
+      for (int u = 0; u < S; ++u) acc[u] = __dadd_rn(acc[u], __dmul_rn(v, q[u]));
     }
 #pragma unroll
     for (int u = 0; u < S; ++u) w[i * S + u] = acc[u];
@@ -271,213 +307,120 @@ __global__ void __launch_bounds__(256) k_spmm(SolveConst c) {
 }
 
 // =====================================================================
-// K2: R1 Gram of x against blocks [b0, b0+gridDim.y-1) and x^T x (last y).
-// Each CTA handles one (row-group, block) pair. Two-level last-CTA:
-// per-block trees, then a side-level finalisation in the very last CTA.
+// K2: R1 Gram of x against blocks [b0, b1). One CTA per (row group, block).
 // =====================================================================
-enum GramMode : int { GM_LANCZOS1 = 0, GM_MAT = 1, GM_CLEAN = 2, GM_ARN1 = 3, GM_ARN2 = 4 };
+enum GramMode : int { GM_J = 0, GM_ALL_W = 1, GM_ALL_X = 2, GM_CLEAN = 3 };
 
-template <int S>
-__device__ void gram_side_finalize(const SolveConst& c, int side, int mode);
-
-// which x does this mode read, and which blocks
 template <int S>
 __device__ inline bool gram_setup(const SolveConst& c, int side, int mode, const double*& x,
-                                  int64_t& b0, int64_t& b1) {
+                                  double*& out, int64_t& b0, int64_t& b1) {
   const DevState* st = c.st;
   if (st->status != RUNNING) return false;
   const SideState& ss = st->side[side];
   const SideConst& sc = c.side[side];
   const int64_t k = ss.blocks;
+  if (mode == GM_CLEAN) {
+    if (ss.stage != ST_NEED_CLEANUP) return false;
+    x = sc.blocks[k];
+    out = sc.coef2;
+    b0 = 0;
+    b1 = k;
+    return true;
+  }
+  if (ss.exhausted || ss.broken) return false;
   switch (mode) {
-    case GM_LANCZOS1:  // pass 1 of a Lanczos step: x = w, blocks J
-      if (ss.exhausted || ss.broken) return false;
+    case GM_J:
       x = sc.w;
+      out = sc.coef;
       b0 = first_block(c, k);
       b1 = k;
       return true;
-    case GM_MAT:  // direct Gram of materialised wx (self only)
-      if (ss.stage != ST_NEED_MAT || ss.cleanup_done == 2) return false;
-      x = sc.wx;
-      b0 = b1 = 0;
-      return true;
-    case GM_CLEAN:  // clean-up Gram of wx vs all blocks (no self)
-      if (ss.stage != ST_NEED_CLEANUP) return false;
-      x = sc.wx;
-      b0 = 0;
-      b1 = k;
-      return true;
-    case GM_ARN1:  // Arnoldi pass 1: x = w vs all blocks (no self)
-      if (ss.exhausted || ss.broken) return false;
+    case GM_ALL_W:
       x = sc.w;
+      out = sc.coef;
       b0 = 0;
       b1 = k;
       return true;
-    case GM_ARN2:  // Arnoldi pass 2: x = wx (= w1) vs all blocks + self
-      if (ss.exhausted || ss.broken) return false;
+    case GM_ALL_X:
       x = sc.wx;
+      out = sc.coef2;
       b0 = 0;
       b1 = k;
       return true;
   }
   return false;
 }
-__device__ inline bool gram_has_self(int mode) {
-  return mode == GM_LANCZOS1 || mode == GM_MAT || mode == GM_ARN2;
-}
-__device__ inline double* gram_coef_out(const SideConst& sc, int mode) {
-  return (mode == GM_CLEAN || mode == GM_ARN2) ? sc.coef2 : sc.coef;
-}
 
 template <int S>
 __global__ void __launch_bounds__(256) k_gram(SolveConst c, int mode) {
   constexpr int NB = S * S;
-  constexpr int NS = S * (S + 1) / 2;
   const int side = blockIdx.z;
   if (side >= c.nsides) return;
   const double* x;
+  double* out;
   int64_t b0, b1;
-  if (!gram_setup<S>(c, side, mode, x, b0, b1)) return;
-  const bool self = gram_has_self(mode);
+  if (!gram_setup<S>(c, side, mode, x, out, b0, b1)) return;
   const SideConst& sc = c.side[side];
-  const int64_t nblk = (b1 - b0) + (self ? 1 : 0);
+  const int64_t nblk = b1 - b0;
   const int64_t by = blockIdx.y;
   if (by >= nblk) return;
   const int64_t cta = blockIdx.x;
   if (cta >= sc.ncta) return;
-  const bool is_self = self && by == nblk - 1;
-  const double* __restrict__ vb = is_self ? x : sc.blocks[b0 + by];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int64_t n = sc.n, nseg = sc.nseg;
-  const int64_t seg_cta0 = cta * kSegsPerCta;
-  const int nvalid_cta = (int)mn64(kSegsPerCta, nseg - seg_cta0);
-  const int64_t seg_w0 = seg_cta0 + warp * kSegsPerWarp;
-  const int nvalid_warp = (int)mx64(0, mn64(kSegsPerWarp, nseg - seg_w0));
+  const int64_t b = b0 + by;
+  const double* __restrict__ vb = sc.blocks[b];
+  NF<S> f;
+  load_nf<S>(sc.nfac, b, f);
+  const int lane = threadIdx.x & 31;
+  const int64_t n = sc.n;
+  const SegGeom g = seg_geom(cta, sc.nseg);
   double* part = sc.part + ((by * sc.ncta + cta) * NB);
-
-  if (!is_self) {
-    OwnerVals<NB> segv[kSegsPerWarp];
+  OwnerVals<NB> segv[kSegsPerWarp];
 #pragma unroll
-    for (int q = 0; q < kSegsPerWarp; ++q) {
-      double acc[NB];
+  for (int q = 0; q < kSegsPerWarp; ++q) {
+    double acc[NB];
 #pragma unroll
-      for (int e = 0; e < NB; ++e) acc[e] = 0.0;
-      if (q < nvalid_warp) {
-        const int64_t base = (seg_w0 + q) * kSeg;
+    for (int e = 0; e < NB; ++e) acc[e] = 0.0;
+    if (q < g.nvalid_warp) {
+      const int64_t base = (g.seg_w0 + q) * kSeg;
 #pragma unroll 4
-        for (int m = 0; m < kLRows; ++m) {
-          const int64_t i = base + lane + 32 * m;
-          if (i < n) {
-            double a[S], y[S];
+      for (int m = 0; m < kLRows; ++m) {
+        const int64_t i = base + lane + 32 * m;
+        if (i < n) {
+          double a[S], y[S];
+          load_vrow<S>(vb, f, i, a);
 #pragma unroll
-            for (int t = 0; t < S; ++t) {
-              a[t] = __ldg(vb + i * S + t);
-              y[t] = __ldg(x + i * S + t);
-            }
+          for (int t = 0; t < S; ++t) y[t] = __ldg(x + i * S + t);
 #pragma unroll
-            for (int u = 0; u < S; ++u)
+          for (int u = 0; u < S; ++u)
 #pragma unroll
-              for (int t = 0; t < S; ++t) acc[u * S + t] = __dadd_rn(acc[u * S + t], __dmul_rn(a[t], y[u]));
-          }
+            for (int t = 0; t < S; ++t)
+              acc[u * S + t] = __dadd_rn(acc[u * S + t], __dmul_rn(a[t], y[u]));
         }
       }
-      seg_butterfly<NB>(acc, segv[q], lane);
     }
-    cta_combine<NB>(segv, nvalid_warp, nvalid_cta, part);
-  } else {
-    OwnerVals<NS> segv[kSegsPerWarp];
-#pragma unroll
-    for (int q = 0; q < kSegsPerWarp; ++q) {
-      double acc[NS];
-#pragma unroll
-      for (int e = 0; e < NS; ++e) acc[e] = 0.0;
-      if (q < nvalid_warp) {
-        const int64_t base = (seg_w0 + q) * kSeg;
-#pragma unroll 4
-        for (int m = 0; m < kLRows; ++m) {
-          const int64_t i = base + lane + 32 * m;
-          if (i < n) {
-            double y[S];
-#pragma unroll
-            for (int t = 0; t < S; ++t) y[t] = __ldg(x + i * S + t);
-            int e = 0;
-#pragma unroll
-            for (int u = 0; u < S; ++u)
-#pragma unroll
-              for (int t = 0; t <= u; ++t) {
-                acc[e] = __dadd_rn(acc[e], __dmul_rn(y[t], y[u]));
-                ++e;
-              }
-          }
-        }
-      }
-      seg_butterfly<NS>(acc, segv[q], lane);
-    }
-    cta_combine<NS>(segv, nvalid_warp, nvalid_cta, part);
+    seg_butterfly<NB>(acc, segv[q], lane);
   }
+  cta_combine<NB>(segv, g.nvalid_warp, g.nvalid_cta, part);
 
   // level 1: the last CTA of this (side, block) reduces over row groups
-  unsigned int* ctr = sc.counter;  // slot 2+by: per-block, slot 0: side
+  unsigned int* ctr = sc.counter;  // slots: 0 side-level, 1 update, 2.. per block
   if (!last_cta_arrive(ctr + 2 + by, (unsigned)sc.ncta)) return;
-  {
-    const int ne = is_self ? NS : NB;
-    for (int e = threadIdx.x; e < ne; e += blockDim.x) {
-      const double v = tree_stream(sc.part + by * sc.ncta * NB + e, sc.ncta, NB);
-      if (is_self) {
-        // unpack upper triangle into the full symmetric gbase
-        int u = 0, t = e;
-        while (t > u) {
-          t -= u + 1;
-          ++u;
-        }
-        c.st->side[side].gbase[u * S + t] = v;
-        c.st->side[side].gbase[t * S + u] = v;
-      } else {
-        gram_coef_out(sc, mode)[(b0 + by) * NB + e] = v;
-      }
-    }
-  }
-  // level 2: the last block-level reducer finalises the side
-  if (!last_cta_arrive(ctr + 0, (unsigned)nblk)) return;
-  if (threadIdx.x == 0) gram_side_finalize<S>(c, side, mode);
-}
-
-template <int S>
-__device__ void gram_side_finalize(const SolveConst& c, int side, int mode) {
-  SideState& st = c.st->side[side];
-  const SideConst& sc = c.side[side];
-  const int64_t k = st.blocks;
-  switch (mode) {
-    case GM_LANCZOS1:
-      st.cleanup_done = 0;
-      finalize_pyth(c, side, sc.coef, first_block(c, k), k);
-      break;
-    case GM_MAT:
-      finalize_direct(c, side, true);
-      break;
-    case GM_CLEAN:
-      break;  // coefficients stored; update kernel follows
-    case GM_ARN1:
-      break;  // update kernel follows
-    case GM_ARN2: {
-      // H column = c1 + c2 (block_krylov.cpp:87-93 folds both passes)
-      // keep c2 for the Pythagorean Gram; coef becomes the H coefficients after.
-      double cc2[kMaxS * kMaxS];
-      (void)cc2;
-      st.cleanup_done = 0;
-      finalize_pyth(c, side, sc.coef2, 0, k);
-      break;
+  for (int e = threadIdx.x; e < NB; e += blockDim.x) {
+    const double v = tree_stream(sc.part + by * sc.ncta * NB + e, sc.ncta, NB);
+    out[b * NB + e] = v;
+    if (mode == GM_ALL_X && c.arnoldi) {
+      // H column = first + second CGS pass (block_krylov.cpp:87-93)
+      const int t = e % S, u = e / S;
+      const double h = __dadd_rn(__ldcg(sc.coef + b * NB + e), v);
+      hcol_ptr(sc, c.st->side[side].steps, u, S)[b * S + t] = h;
     }
   }
 }
 
 // =====================================================================
-// x_out = x_in - sum_{b in [b0,b1)} V_b c_b  (+ R1 self Gram of x_out)
-// modes: UM_MAT (wx = base - V cc, then direct Gram),
-//        UM_CLEAN (wx -= V d over all blocks, then direct Gram),
-//        UM_ARN (wx = w - V c1 over all blocks; Gram vs blocks follows)
+// x_out = x_in - sum_{b in [b0,b1)} V_b c_b (+ R1 Gram of x_out, finalise)
 // =====================================================================
-enum UpdMode : int { UM_MAT = 0, UM_CLEAN = 1, UM_ARN = 2 };
+enum UpdMode : int { UM_LANCZOS = 0, UM_FIRST = 1, UM_SECOND = 2, UM_CLEAN = 3, UM_INIT = 4 };
 
 template <int S>
 __global__ void __launch_bounds__(256) k_update(SolveConst c, int mode) {
@@ -485,46 +428,57 @@ __global__ void __launch_bounds__(256) k_update(SolveConst c, int mode) {
   const int side = blockIdx.z;
   if (side >= c.nsides) return;
   const DevState* st = c.st;
-  if (st->status != RUNNING) return;
+  if (mode != UM_INIT && st->status != RUNNING) return;
   const SideState& ss = st->side[side];
   const SideConst& sc = c.side[side];
   const int64_t k = ss.blocks;
   const double* xin;
-  const double* coef;
-  int64_t b0, b1;
+  const double* coef = sc.coef;
+  double* xout;
+  int64_t b0 = 0, b1 = 0;
   bool gram = true;
-  if (mode == UM_MAT) {
-    if (!(ss.stage == ST_NEED_MAT || ss.stage == ST_NEED_MAT_CLEANUP)) return;
-    // base = w (Lanczos) or w1 (Arnoldi / full reorth, already in wx)
-    xin = c.arnoldi ? sc.wx : sc.w;
-    coef = c.arnoldi ? sc.coef2 : sc.coef;
-    b0 = c.arnoldi ? 0 : first_block(c, k);
-    b1 = k;
-    gram = (ss.stage == ST_NEED_MAT && ss.cleanup_done != 2);
-  } else if (mode == UM_CLEAN) {
-    if (ss.stage != ST_NEED_CLEANUP) return;
-    xin = sc.wx;
-    coef = sc.coef2;
-    b0 = 0;
-    b1 = k;
-  } else {
-    if (ss.exhausted || ss.broken) return;
-    xin = sc.w;
-    coef = sc.coef;
-    b0 = 0;
-    b1 = k;
-    gram = false;
+  switch (mode) {
+    case UM_LANCZOS:
+      if (ss.exhausted || ss.broken) return;
+      xin = sc.w;
+      xout = sc.blocks[k];
+      b0 = first_block(c, k);
+      b1 = k;
+      break;
+    case UM_FIRST:
+      if (ss.exhausted || ss.broken) return;
+      xin = sc.w;
+      xout = sc.wx;
+      b0 = first_block(c, k);
+      b1 = k;
+      gram = false;
+      break;
+    case UM_SECOND:
+      if (ss.exhausted || ss.broken) return;
+      xin = sc.wx;
+      xout = sc.blocks[k];
+      coef = sc.coef2;
+      b0 = 0;
+      b1 = k;
+      break;
+    case UM_CLEAN:
+      if (ss.stage != ST_NEED_CLEANUP) return;
+      xin = sc.blocks[k];
+      xout = sc.blocks[k];
+      coef = sc.coef2;
+      b0 = 0;
+      b1 = k;
+      break;
+    default:  // UM_INIT: U_0 = transposed C
+      xin = sc.wx;
+      xout = sc.blocks[0];
+      break;
   }
   const int64_t cta = blockIdx.x;
   if (cta >= sc.ncta) return;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int64_t n = sc.n, nseg = sc.nseg;
-  const int64_t seg_cta0 = cta * kSegsPerCta;
-  const int nvalid_cta = (int)mn64(kSegsPerCta, nseg - seg_cta0);
-  const int64_t seg_w0 = seg_cta0 + warp * kSegsPerWarp;
-  const int nvalid_warp = (int)mx64(0, mn64(kSegsPerWarp, nseg - seg_w0));
-  double* __restrict__ xout = sc.wx;
-  __shared__ double cs[kMaxS * kMaxS * 16];
+  const int lane = threadIdx.x & 31;
+  const int64_t n = sc.n;
+  const SegGeom g = seg_geom(cta, sc.nseg);
 
   OwnerVals<NS> segv[kSegsPerWarp];
 #pragma unroll 1
@@ -532,9 +486,9 @@ __global__ void __launch_bounds__(256) k_update(SolveConst c, int mode) {
     double acc[NS];
 #pragma unroll
     for (int e = 0; e < NS; ++e) acc[e] = 0.0;
-    if (q < nvalid_warp) {
-      const int64_t base = (seg_w0 + q) * kSeg;
-#pragma unroll 1
+    if (q < g.nvalid_warp) {
+      const int64_t base = (g.seg_w0 + q) * kSeg;
+#pragma unroll 2
       for (int m = 0; m < kLRows; ++m) {
         const int64_t i = base + lane + 32 * m;
         if (i < n) {
@@ -542,11 +496,11 @@ __global__ void __launch_bounds__(256) k_update(SolveConst c, int mode) {
 #pragma unroll
           for (int u = 0; u < S; ++u) y[u] = __ldcg(xin + i * S + u);
           for (int64_t b = b0; b < b1; ++b) {
-            const double* vb = sc.blocks[b];
-            const double* cb = coef + b * (S * S);
+            NF<S> f;
+            load_nf<S>(sc.nfac, b, f);
             double a[S];
-#pragma unroll
-            for (int t = 0; t < S; ++t) a[t] = __ldg(vb + i * S + t);
+            load_vrow<S>(sc.blocks[b], f, i, a);
+            const double* cb = coef + b * (S * S);
 #pragma unroll
             for (int u = 0; u < S; ++u) {
               double tmp = 0.0;
@@ -570,51 +524,35 @@ __global__ void __launch_bounds__(256) k_update(SolveConst c, int mode) {
     }
     if (gram) seg_butterfly<NS>(acc, segv[q], lane);
   }
-  (void)cs;
   if (!gram) return;
-  double* part = sc.part + cta * NS;
-  cta_combine<NS>(segv, nvalid_warp, nvalid_cta, part);
+  cta_combine<NS>(segv, g.nvalid_warp, g.nvalid_cta, sc.part + cta * NS);
   if (!last_cta_arrive(sc.counter + 1, (unsigned)sc.ncta)) return;
+  SideState& sst = c.st->side[side];
   for (int e = threadIdx.x; e < NS; e += blockDim.x) {
     const double v = tree_stream(sc.part + e, sc.ncta, NS);
-    int u = 0, t = e;
-    while (t > u) {
-      t -= u + 1;
-      ++u;
-    }
-    c.st->side[side].gbase[u * S + t] = v;
-    c.st->side[side].gbase[t * S + u] = v;
+    int t, u;
+    unpack_tri(e, t, u);
+    sst.gbase[u * S + t] = v;
+    sst.gbase[t * S + u] = v;
   }
   __syncthreads();
   if (threadIdx.x == 0) {
-    SideState& sst = c.st->side[side];
-    if (mode == UM_MAT) {
-      finalize_direct(c, side, true);
+    if (mode == UM_INIT) {
+      finalize_init(c, side);
     } else if (mode == UM_CLEAN) {
-      sst.paths[3]++;
-      sst.cleanup_done = 1;
+      sst.paths[2]++;
       finalize_direct(c, side, false);
+    } else {
+      finalize_direct(c, side, true);
     }
   }
 }
 
-// Materialise only (no Gram): NEED_MAT with Householder marker, or clean-up prep.
-// Implemented by k_update(UM_MAT) with gram=false; stage transition here:
-static __global__ void k_mat_transition(SolveConst c) {
-  const int side = threadIdx.x;
-  if (side >= c.nsides || c.st->status != RUNNING) return;
-  SideState& st = c.st->side[side];
-  if (st.stage == ST_NEED_MAT && st.cleanup_done == 2) st.stage = ST_NEED_HH;
-  else if (st.stage == ST_NEED_MAT_CLEANUP) st.stage = ST_NEED_CLEANUP;
-}
-
 // =====================================================================
-// Rare path: single-CTA Householder QR of wx (decompositions.cpp:16-78 with
-// R1 reductions). Writes Q to qh (row-interleaved) and R to the side state.
+// Rare path: single-CTA Householder QR (decompositions.cpp:16-78 with R1 dots)
 // =====================================================================
 static __device__ double cta_r1_dot(const double* x, int sx, int cx, const double* y, int sy, int cy,
-                             int64_t n, int64_t row0, double* segbuf) {
-  // R1 over rows [row0, n) of x(i,cx)*y(i,cy); segment partials by warps, then stream tree.
+                                    int64_t n, int64_t row0, double* segbuf) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const int64_t nseg = (n + kSeg - 1) / kSeg;
   for (int64_t g = warp; g < nseg; g += nw) {
@@ -680,7 +618,6 @@ __device__ void householder_cta(double* W, double* Q, int64_t n, double* R, doub
       __syncthreads();
     }
   }
-  // Q accumulation
   for (int64_t i = threadIdx.x; i < n; i += blockDim.x)
     for (int cc = 0; cc < S; ++cc) Q[i * S + cc] = (i == cc && cc < p) ? 1.0 : 0.0;
   __threadfence_block();
@@ -725,95 +662,42 @@ __device__ void householder_cta(double* W, double* Q, int64_t n, double* R, doub
   }
 }
 
-// Householder of wx (work, destroyed) for sides whose stage asks for it.
+// which: 0 first-pass NEED_HH, 1 NEED_HH2 after clean-up, 2 init (U_0)
 template <int S>
-__global__ void __launch_bounds__(1024) k_householder(SolveConst c, int which /*0: HH, 1: HH2*/) {
+__global__ void __launch_bounds__(1024) k_householder(SolveConst c, int which) {
   const int side = blockIdx.x;
-  if (side >= c.nsides || c.st->status != RUNNING) return;
+  if (side >= c.nsides) return;
+  if (which != 2 && c.st->status != RUNNING) return;
   SideState& st = c.st->side[side];
-  const int want = which == 0 ? ST_NEED_HH : ST_NEED_HH2;
+  const int want = which == 0 ? ST_NEED_HH : (which == 1 ? ST_NEED_HH2 : ST_INIT_HH);
   if (st.stage != want) return;
   const SideConst& sc = c.side[side];
-  __shared__ double R[kMaxS * kMaxS];
-  for (int64_t i = threadIdx.x; i < sc.n * S; i += blockDim.x) sc.hw[i] = sc.wx[i];
+  const int64_t k = which == 2 ? 0 : st.blocks;
+  double* cand = sc.blocks[k];
+  for (int64_t i = threadIdx.x; i < sc.n * S; i += blockDim.x) sc.hw[i] = cand[i];
   __syncthreads();
+  __shared__ double R[kMaxS * kMaxS];
   householder_cta<S>(sc.hw, sc.qh, sc.n, R, sc.part);
+  __shared__ int accept;
   if (threadIdx.x == 0) {
     for (int e = 0; e < S * S; ++e) st.R[e] = R[e];
     jacobi_extremes(st.R, S, S, &st.smax, &st.smin);
-    if (which == 0) st.paths[2]++;
-    classify(c, side, which == 0, ST_GROW_HH);
-  }
-}
-
-// =====================================================================
-// K3: write the new block  (block_krylov.cpp:139-144 append_block)
-// =====================================================================
-template <int S>
-__global__ void __launch_bounds__(256) k_pass2(SolveConst c) {
-  const int side = blockIdx.y;
-  if (side >= c.nsides || c.st->status != RUNNING) return;
-  const SideState& st = c.st->side[side];
-  const int stage = st.stage;
-  if (stage != ST_GROW_PYTH && stage != ST_GROW_WX && stage != ST_GROW_HH) return;
-  const SideConst& sc = c.side[side];
-  const int64_t knew = st.blocks - 1;  // committed already
-  double* __restrict__ out = sc.blocks[knew];
-  const int64_t n = sc.n;
-  __shared__ double Rs[S * S];
-  __shared__ double cs[2 * S * S];
-  if (threadIdx.x < S * S) Rs[threadIdx.x] = st.R[threadIdx.x];
-  const int64_t kold = knew;  // blocks before this step
-  const int64_t b0 = c.arnoldi ? 0 : first_block(c, kold);
-  const double* coef = c.arnoldi ? sc.coef2 : sc.coef;
-  const double* base = c.arnoldi ? sc.wx : sc.w;
-  __syncthreads();
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    double y[S];
-    if (stage == ST_GROW_HH) {
-#pragma unroll
-      for (int u = 0; u < S; ++u) out[i * S + u] = sc.qh[i * S + u];
-      continue;
-    }
-    if (stage == ST_GROW_WX) {
-#pragma unroll
-      for (int u = 0; u < S; ++u) y[u] = __ldcg(sc.wx + i * S + u);
+    if (which == 2) {
+      set_nfac(sc, 0, S, st.R, true);
+      accept = 1;
     } else {
-#pragma unroll
-      for (int u = 0; u < S; ++u) y[u] = __ldcg(base + i * S + u);
-      for (int64_t b = b0; b < kold; ++b) {
-        const double* vb = sc.blocks[b];
-        const double* cb = coef + b * (S * S);
-        double a[S];
-#pragma unroll
-        for (int t = 0; t < S; ++t) a[t] = __ldg(vb + i * S + t);
-#pragma unroll
-        for (int u = 0; u < S; ++u) {
-          double tmp = 0.0;
-#pragma unroll
-          for (int t = 0; t < S; ++t) tmp = __dadd_rn(tmp, __dmul_rn(a[t], __ldg(cb + u * S + t)));
-          y[u] = __dsub_rn(y[u], tmp);
-        }
-      }
+      if (which == 0) st.paths[1]++;
+      classify(c, side, which == 0, ST_GROW_HH);
+      accept = st.stage == ST_GROW_HH;
     }
-    double q[S];
-#pragma unroll
-    for (int u = 0; u < S; ++u) {
-      double acc = y[u];
-#pragma unroll
-      for (int t = 0; t < u; ++t) acc = __dsub_rn(acc, __dmul_rn(q[t], Rs[u * S + t]));
-      q[u] = __ddiv_rn(acc, Rs[u * S + u]);
-    }
-#pragma unroll
-    for (int u = 0; u < S; ++u) out[i * S + u] = q[u];
   }
-  (void)cs;
+  __syncthreads();
+  if (accept)
+    for (int64_t i = threadIdx.x; i < sc.n * S; i += blockDim.x) cand[i] = sc.qh[i];
 }
 
 // =====================================================================
-// Basis initialisation (block_krylov.cpp:27-52): C (column-major, n x s) is
-// transposed into wx, R1 Gram, CholQR with Householder fallback, rank check.
+// Initialisation (block_krylov.cpp:27-52; factorized_solvers.cpp:121-131)
 // =====================================================================
 template <int S>
 __global__ void k_init_transpose(SolveConst c, const double* c1, const double* c2) {
@@ -827,157 +711,19 @@ __global__ void k_init_transpose(SolveConst c, const double* c1, const double* c
     for (int u = 0; u < S; ++u) sc.wx[i * S + u] = src[u * sc.n + i];
 }
 
-template <int S>
-__global__ void __launch_bounds__(256) k_init_gram(SolveConst c) {
-  constexpr int NS = S * (S + 1) / 2;
-  const int side = blockIdx.z;
-  if (side >= c.nsides) return;
-  const SideConst& sc = c.side[side];
-  const int64_t cta = blockIdx.x;
-  if (cta >= sc.ncta) return;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int64_t n = sc.n, nseg = sc.nseg;
-  const int64_t seg_cta0 = cta * kSegsPerCta;
-  const int nvalid_cta = (int)mn64(kSegsPerCta, nseg - seg_cta0);
-  const int64_t seg_w0 = seg_cta0 + warp * kSegsPerWarp;
-  const int nvalid_warp = (int)mx64(0, mn64(kSegsPerWarp, nseg - seg_w0));
-  const double* x = sc.wx;
-  OwnerVals<NS> segv[kSegsPerWarp];
-  for (int q = 0; q < kSegsPerWarp; ++q) {
-    double acc[NS];
-#pragma unroll
-    for (int e = 0; e < NS; ++e) acc[e] = 0.0;
-    if (q < nvalid_warp) {
-      const int64_t base = (seg_w0 + q) * kSeg;
-      for (int m = 0; m < kLRows; ++m) {
-        const int64_t i = base + lane + 32 * m;
-        if (i < n) {
-          double y[S];
-#pragma unroll
-          for (int t = 0; t < S; ++t) y[t] = x[i * S + t];
-          int e = 0;
-#pragma unroll
-          for (int u = 0; u < S; ++u)
-#pragma unroll
-            for (int t = 0; t <= u; ++t) {
-              acc[e] = __dadd_rn(acc[e], __dmul_rn(y[t], y[u]));
-              ++e;
-            }
-        }
-      }
-    }
-    seg_butterfly<NS>(acc, segv[q], lane);
-  }
-  cta_combine<NS>(segv, nvalid_warp, nvalid_cta, sc.part + cta * NS);
-  if (!last_cta_arrive(sc.counter + 1, (unsigned)sc.ncta)) return;
-  SideState& st = c.st->side[side];
-  for (int e = threadIdx.x; e < NS; e += blockDim.x) {
-    const double v = tree_stream(sc.part + e, sc.ncta, NS);
-    int u = 0, t = e;
-    while (t > u) {
-      t -= u + 1;
-      ++u;
-    }
-    st.gbase[u * S + t] = v;
-    st.gbase[t * S + u] = v;
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    // Pythagorean step with no prior blocks: G' = G; guard G(u,u) > 2^-10 G(u,u)
-    bool ok = true;
-    for (int u = 0; u < S; ++u)
-      if (!(st.gbase[u * S + u] > __dmul_rn(st.gbase[u * S + u], kPythGuard))) ok = false;
-    if (ok) ok = cholesky_upper(st.gbase, S, st.R);
-    if (ok) {
-      jacobi_extremes(st.R, S, S, &st.smax, &st.smin);
-      if (st.smin < __dmul_rn(kHHRatio, st.smax)) {
-        st.stage = ST_NEED_HH;  // Householder directly on C
-        st.paths[2]++;
-      } else {
-        st.stage = ST_GROW_WX;
-        st.paths[0]++;
-      }
-    } else {
-      // direct Gram of the same data == gbase: repeat the decision (explicit path)
-      ok = cholesky_upper(st.gbase, S, st.R);
-      if (ok) {
-        jacobi_extremes(st.R, S, S, &st.smax, &st.smin);
-        if (st.smin < __dmul_rn(kHHRatio, st.smax)) ok = false;
-      }
-      if (ok) {
-        st.stage = ST_GROW_WX;
-        st.paths[1]++;
-      } else {
-        st.stage = ST_NEED_HH;
-        st.paths[2]++;
-      }
-    }
-  }
-}
-
-template <int S>
-__global__ void __launch_bounds__(1024) k_init_householder(SolveConst c) {
-  const int side = blockIdx.x;
-  if (side >= c.nsides) return;
-  SideState& st = c.st->side[side];
-  if (st.stage != ST_NEED_HH) return;
-  const SideConst& sc = c.side[side];
-  __shared__ double R[kMaxS * kMaxS];
-  householder_cta<S>(sc.wx, sc.qh, sc.n, R, sc.part);
-  if (threadIdx.x == 0) {
-    for (int e = 0; e < S * S; ++e) st.R[e] = R[e];
-    jacobi_extremes(st.R, S, S, &st.smax, &st.smin);
-    st.stage = ST_GROW_HH;
-  }
-}
-
-// V_0 = C R^-1 (or Q_h); rank check (block_krylov.cpp:38-40)
-template <int S>
-__global__ void k_init_write(SolveConst c) {
-  const int side = blockIdx.y;
-  if (side >= c.nsides) return;
-  const SideState& st = c.st->side[side];
-  const SideConst& sc = c.side[side];
-  if (st.smin < __dmul_rn(1e-12, st.smax) || st.smax == 0.0) return;  // rank deficient
-  double* out = sc.blocks[0];
-  __shared__ double Rs[S * S];
-  if (threadIdx.x < S * S) Rs[threadIdx.x] = st.R[threadIdx.x];
-  __syncthreads();
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < sc.n;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    if (st.stage == ST_GROW_HH) {
-#pragma unroll
-      for (int u = 0; u < S; ++u) out[i * S + u] = sc.qh[i * S + u];
-      continue;
-    }
-    double q[S];
-#pragma unroll
-    for (int u = 0; u < S; ++u) {
-      double acc = sc.wx[i * S + u];
-#pragma unroll
-      for (int t = 0; t < u; ++t) acc = __dsub_rn(acc, __dmul_rn(q[t], Rs[u * S + t]));
-      q[u] = __ddiv_rn(acc, Rs[u * S + u]);
-    }
-#pragma unroll
-    for (int u = 0; u < S; ++u) out[i * S + u] = q[u];
-  }
-}
-
-// R_0 = R_L R_R^T, P_0 = R_0, rho_0 = <R_0,R_0> (factorized_solvers.cpp:121-131)
+// R_0 = R_L R_R^T, P_0 = R_0, rho_0 = <R_0,R_0> (R2 contract, one tile)
 static __global__ void k_core_init(SolveConst c) {
   DevState* st = c.st;
   const int s = c.s;
   if (threadIdx.x != 0) return;
   const SideState& a = st->side[0];
   const SideState& b = st->side[c.nsides > 1 ? 1 : 0];
-  bool rd = false;
   for (int sd = 0; sd < c.nsides; ++sd) {
     const SideState& x = st->side[sd];
-    if (x.smin < __dmul_rn(1e-12, x.smax) || x.smax == 0.0) rd = true;
-  }
-  if (rd) {
-    st->status = RANKDEF;
-    return;
+    if (x.smin < __dmul_rn(1e-12, x.smax) || x.smax == 0.0) {
+      st->status = RANKDEF;
+      return;
+    }
   }
   for (int sd = 0; sd < c.nsides; ++sd) {
     st->side[sd].blocks = 1;
@@ -992,12 +738,11 @@ static __global__ void k_core_init(SolveConst c) {
       c.P[0][j * c.ld + i] = acc;
       if (c.Rs) c.Rs[j * s + i] = acc;
     }
-  // R2 contract over the s x s window (single tile)
   double lane[32];
   for (int l = 0; l < 32; ++l) {
     double acc = 0.0;
     if (l < s)
-      for (int j = 0; j < s && j < 32; ++j) acc = __dadd_rn(acc, __dmul_rn(c.R[j * c.ld + l], c.R[j * c.ld + l]));
+      for (int j = 0; j < s; ++j) acc = __dadd_rn(acc, __dmul_rn(c.R[j * c.ld + l], c.R[j * c.ld + l]));
     lane[l] = acc;
   }
   for (int d = 16; d >= 1; d >>= 1) {
@@ -1021,7 +766,6 @@ static __global__ void k_core_init(SolveConst c) {
 // =====================================================================
 // K4: CG core kernels (factorized_solvers.cpp:150-189 fused)
 // =====================================================================
-// Band coefficient H(i,l) for |b(i)-b(l)| <= 1 from the Lanczos band store.
 __device__ __forceinline__ double band_at(const double* hband, int s, int64_t i, int64_t l) {
   const int64_t bi = i / s, bl = l / s;
   const int64_t d = bi - bl + 1;
@@ -1030,12 +774,10 @@ __device__ __forceinline__ double band_at(const double* hband, int s, int64_t i,
 
 template <int S>
 struct CgTile {
-  static constexpr int H = 2 * S;           // halo
-  static constexpr int D = kTile + 2 * H;   // staged edge
+  static constexpr int H = 2 * S;
+  static constexpr int D = kTile + 2 * H;
 };
 
-// Load the staged P region (rows [i0-H, i0+32+H) x cols [j0-H, j0+32+H)).
-// mode 0: P = R (k==0) or R + beta*Pprev; mode 1: P read from Pcur.
 template <int S>
 __device__ void stage_p(double* sp, const SolveConst& c, int64_t i0, int64_t j0, int64_t rows_p,
                         int64_t cols_p, int mode, const double* Pprev, const double* Pcur, double beta,
@@ -1058,7 +800,6 @@ __device__ void stage_p(double* sp, const SolveConst& c, int64_t i0, int64_t j0,
   }
 }
 
-// q(i,j) from the staged P (local coords), bands of V (hv) and W (hw)
 template <int S>
 __device__ __forceinline__ double image_at(const double* sp, const double* hv, const double* hw,
                                            int64_t i, int64_t j, int64_t i0, int64_t j0, int64_t pr,
@@ -1097,7 +838,6 @@ __device__ __forceinline__ double image_at(const double* sp, const double* hv, c
   return hasH ? hpart : (hasG ? gpart : 0.0);
 }
 
-// tile partial: f values in smem f[c][row]; warp 0 sums sequentially, butterflies.
 __device__ __forceinline__ double tile_reduce(const double* f, int nrows, int ncols) {
   double acc = 0.0;
   const int lane = threadIdx.x & 31;
@@ -1106,7 +846,6 @@ __device__ __forceinline__ double tile_reduce(const double* f, int nrows, int nc
   return butterfly(acc);
 }
 
-// R2 final: per tile column tree over ti, then over tj (streamed).
 static __device__ double r2_final(const double* part, int64_t nti, int64_t ntj, double* scratch) {
   for (int64_t tj = threadIdx.x; tj < ntj; tj += blockDim.x)
     scratch[tj] = tree_stream(part + tj * nti, nti, 1);
@@ -1186,8 +925,7 @@ __global__ void __launch_bounds__(256) k_cg_a(SolveConst c) {
   const double denom = r2_final(c.cpart, nti, ntj, scr);
   if (threadIdx.x == 0) {
     st->denom = denom;
-    // breakdown guard (factorized_solvers.cpp:155-160)
-    if (fabs(denom) < __dmul_rn(c.tol, st->rho)) {
+    if (fabs(denom) < __dmul_rn(c.tol, st->rho)) {  // factorized_solvers.cpp:155-160
       st->status = BREAKDOWN;
       c.hist_rel[k + 1] = c.hist_rel[k];
       c.hist_tb[k + 1] = (double)globaltimer();
@@ -1265,7 +1003,7 @@ __global__ void __launch_bounds__(256) k_cg_b(SolveConst c) {
     st->rows_p = rows_q;
     st->cols_p = cols_q;
     st->k = k + 1;
-    if (norm_r <= __dmul_rn(st->norm_r0, c.eps)) {
+    if (norm_r <= __dmul_rn(st->norm_r0, c.eps)) {  // factorized_solvers.cpp:173-178
       st->status = CONVERGED;
       return;
     }
@@ -1276,9 +1014,8 @@ __global__ void __launch_bounds__(256) k_cg_b(SolveConst c) {
 }
 
 // =====================================================================
-// launchers
+// standalone kernels: SpMM (parity tests), export with normalisation
 // =====================================================================
-// standalone SpMM for parity tests (row-interleaved x, y)
 template <int S>
 __global__ void k_spmm_plain(const int32_t* rp, const int32_t* ci, const double* val,
                              const double* x, double* y, int64_t n) {
@@ -1297,6 +1034,18 @@ __global__ void k_spmm_plain(const int32_t* rp, const int32_t* ci, const double*
     for (int u = 0; u < S; ++u) y[i * S + u] = acc[u];
   }
 }
+template <int S>
+__global__ void k_export_block(const double* blk, const double* nfac, int64_t b, double* out, int64_t n) {
+  NF<S> f;
+  load_nf<S>(nfac, b, f);
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    double q[S];
+    load_vrow<S>(blk, f, i, q);
+#pragma unroll
+    for (int u = 0; u < S; ++u) out[u * n + i] = q[u];
+  }
+}
 
 static int rows_grid(int64_t n) {
   int64_t g = (n + 255) / 256;
@@ -1312,19 +1061,21 @@ static void dims(const SolveConst& c, int64_t& nmax, int64_t& cmax) {
   }
 }
 
-// Per-S launchers (explicitly instantiated, one translation unit per S).
+// ---- per-S launchers (explicitly instantiated, one translation unit per S) ----
 #ifdef SK_INST_COMMON
 template <int S>
 struct Launch {
   static void init(const SolveConst& c, const double* dc1, const double* dc2, cudaStream_t st);
   static void spmm(const SolveConst& c, cudaStream_t st);
-  static void gram_lanczos(const SolveConst& c, cudaStream_t st);
-  static void rare(const SolveConst& c, int64_t kmax_blocks, cudaStream_t st);
-  static void pass2(const SolveConst& c, cudaStream_t st);
+  static void gram(const SolveConst& c, int mode, int64_t nblk, cudaStream_t st);
+  static void update(const SolveConst& c, int mode, cudaStream_t st);
+  static void householder(const SolveConst& c, int which, cudaStream_t st);
   static void cg_a(const SolveConst& c, int64_t rmax, cudaStream_t st);
   static void cg_b(const SolveConst& c, int64_t rmax, cudaStream_t st);
   static void spmm_plain(const int32_t* rp, const int32_t* ci, const double* val, const double* x,
                          double* y, int64_t n, cudaStream_t st);
+  static void export_block(const double* blk, const double* nfac, int64_t b, double* out, int64_t n,
+                           cudaStream_t st);
 };
 #else
 template <int S>
@@ -1332,42 +1083,27 @@ struct Launch {
   static void init(const SolveConst& c, const double* dc1, const double* dc2, cudaStream_t st) {
     int64_t nmax, cmax;
     dims(c, nmax, cmax);
-    dim3 g1(rows_grid(nmax), c.nsides);
-    k_init_transpose<S><<<g1, 256, 0, st>>>(c, dc1, dc2);
-    dim3 g2((unsigned)cmax, 1, c.nsides);
-    k_init_gram<S><<<g2, 256, 0, st>>>(c);
-    k_init_householder<S><<<c.nsides, 1024, 0, st>>>(c);
-    k_init_write<S><<<g1, 256, 0, st>>>(c);
+    k_init_transpose<S><<<dim3(rows_grid(nmax), c.nsides), 256, 0, st>>>(c, dc1, dc2);
+    k_update<S><<<dim3((unsigned)cmax, 1, c.nsides), 256, 0, st>>>(c, (int)UM_INIT);
+    k_householder<S><<<c.nsides, 1024, 0, st>>>(c, 2);
   }
   static void spmm(const SolveConst& c, cudaStream_t st) {
     int64_t nmax, cmax;
     dims(c, nmax, cmax);
-    dim3 g1(rows_grid(nmax), c.nsides);
-    k_spmm<S><<<g1, 256, 0, st>>>(c);
+    k_spmm<S><<<dim3(rows_grid(nmax), c.nsides), 256, 0, st>>>(c);
   }
-  static void gram_lanczos(const SolveConst& c, cudaStream_t st) {
+  static void gram(const SolveConst& c, int mode, int64_t nblk, cudaStream_t st) {
     int64_t nmax, cmax;
     dims(c, nmax, cmax);
-    dim3 gg((unsigned)cmax, 3, c.nsides);
-    k_gram<S><<<gg, 256, 0, st>>>(c, (int)GM_LANCZOS1);
+    k_gram<S><<<dim3((unsigned)cmax, (unsigned)(nblk > 0 ? nblk : 1), c.nsides), 256, 0, st>>>(c, mode);
   }
-  static void rare(const SolveConst& c, int64_t kmax_blocks, cudaStream_t st) {
+  static void update(const SolveConst& c, int mode, cudaStream_t st) {
     int64_t nmax, cmax;
     dims(c, nmax, cmax);
-    dim3 gu((unsigned)cmax, 1, c.nsides);
-    k_update<S><<<gu, 256, 0, st>>>(c, (int)UM_MAT);
-    k_mat_transition<<<1, 32, 0, st>>>(c);
-    k_householder<S><<<c.nsides, 1024, 0, st>>>(c, 0);
-    dim3 gc((unsigned)cmax, (unsigned)(kmax_blocks > 0 ? kmax_blocks : 1), c.nsides);
-    k_gram<S><<<gc, 256, 0, st>>>(c, (int)GM_CLEAN);
-    k_update<S><<<gu, 256, 0, st>>>(c, (int)UM_CLEAN);
-    k_householder<S><<<c.nsides, 1024, 0, st>>>(c, 1);
+    k_update<S><<<dim3((unsigned)cmax, 1, c.nsides), 256, 0, st>>>(c, mode);
   }
-  static void pass2(const SolveConst& c, cudaStream_t st) {
-    int64_t nmax, cmax;
-    dims(c, nmax, cmax);
-    dim3 g1(rows_grid(nmax), c.nsides);
-    k_pass2<S><<<g1, 256, 0, st>>>(c);
+  static void householder(const SolveConst& c, int which, cudaStream_t st) {
+    k_householder<S><<<c.nsides, 1024, 0, st>>>(c, which);
   }
   static void cg_a(const SolveConst& c, int64_t rmax, cudaStream_t st) {
     const unsigned nt = (unsigned)((rmax + kTile - 1) / kTile);
@@ -1381,8 +1117,11 @@ struct Launch {
                          double* y, int64_t n, cudaStream_t st) {
     k_spmm_plain<S><<<rows_grid(n), 256, 0, st>>>(rp, ci, val, x, y, n);
   }
+  static void export_block(const double* blk, const double* nfac, int64_t b, double* out, int64_t n,
+                           cudaStream_t st) {
+    k_export_block<S><<<rows_grid(n), 256, 0, st>>>(blk, nfac, b, out, n);
+  }
 };
-
 #endif  // SK_INST_COMMON
 
 #ifdef SK_INST_S
@@ -1394,39 +1133,58 @@ static int g_launches = 0;
 int launch_count() { return g_launches; }
 void launch_count_reset() { g_launches = 0; }
 
-#define SK_DISPATCH_S(s, CALL)                  \
-  switch (s) {                                  \
-    case 1: Launch<1>::CALL; break;             \
-    case 2: Launch<2>::CALL; break;             \
-    case 3: Launch<3>::CALL; break;             \
-    case 4: Launch<4>::CALL; break;             \
-    case 5: Launch<5>::CALL; break;             \
-    case 6: Launch<6>::CALL; break;             \
-    case 7: Launch<7>::CALL; break;             \
-    case 8: Launch<8>::CALL; break;             \
-    default: break;                             \
+#define SK_DISPATCH_S(s, CALL)      \
+  switch (s) {                      \
+    case 1: Launch<1>::CALL; break; \
+    case 2: Launch<2>::CALL; break; \
+    case 3: Launch<3>::CALL; break; \
+    case 4: Launch<4>::CALL; break; \
+    case 5: Launch<5>::CALL; break; \
+    case 6: Launch<6>::CALL; break; \
+    case 7: Launch<7>::CALL; break; \
+    case 8: Launch<8>::CALL; break; \
+    default: break;                 \
   }
 
 void launch_init(const SolveConst& c, const double* dc1, const double* dc2, cudaStream_t st) {
   SK_DISPATCH_S(c.s, init(c, dc1, dc2, st));
   k_core_init<<<1, 32, 0, st>>>(c);
-  g_launches += 5;
+  g_launches += 4;
 }
 void launch_spmm(const SolveConst& c, cudaStream_t st) {
   SK_DISPATCH_S(c.s, spmm(c, st));
   g_launches += 1;
 }
-void launch_gram_lanczos(const SolveConst& c, cudaStream_t st) {
-  SK_DISPATCH_S(c.s, gram_lanczos(c, st));
+void launch_lanczos_gram(const SolveConst& c, cudaStream_t st) {
+  SK_DISPATCH_S(c.s, gram(c, (int)GM_J, 2, st));
   g_launches += 1;
+}
+void launch_lanczos_update(const SolveConst& c, int64_t kmax_blocks, cudaStream_t st) {
+  if (c.full_reorth) {
+    SK_DISPATCH_S(c.s, update(c, (int)UM_FIRST, st));
+    SK_DISPATCH_S(c.s, gram(c, (int)GM_ALL_X, kmax_blocks, st));
+    SK_DISPATCH_S(c.s, update(c, (int)UM_SECOND, st));
+    g_launches += 3;
+  } else {
+    SK_DISPATCH_S(c.s, update(c, (int)UM_LANCZOS, st));
+    g_launches += 1;
+  }
 }
 void launch_rare(const SolveConst& c, int64_t kmax_blocks, cudaStream_t st) {
-  SK_DISPATCH_S(c.s, rare(c, kmax_blocks, st));
-  g_launches += 6;
+  SK_DISPATCH_S(c.s, householder(c, 0, st));
+  SK_DISPATCH_S(c.s, gram(c, (int)GM_CLEAN, kmax_blocks, st));
+  SK_DISPATCH_S(c.s, update(c, (int)UM_CLEAN, st));
+  SK_DISPATCH_S(c.s, householder(c, 1, st));
+  g_launches += 4;
 }
-void launch_pass2(const SolveConst& c, cudaStream_t st) {
-  SK_DISPATCH_S(c.s, pass2(c, st));
-  g_launches += 1;
+void launch_arnoldi_ext(const SolveConst& c, int64_t kmax_blocks, cudaStream_t st) {
+  SK_DISPATCH_S(c.s, spmm(c, st));
+  SK_DISPATCH_S(c.s, gram(c, (int)GM_ALL_W, kmax_blocks, st));
+  SK_DISPATCH_S(c.s, update(c, (int)UM_FIRST, st));
+  SK_DISPATCH_S(c.s, gram(c, (int)GM_ALL_X, kmax_blocks, st));
+  SK_DISPATCH_S(c.s, update(c, (int)UM_SECOND, st));
+  SK_DISPATCH_S(c.s, householder(c, 0, st));
+  g_launches += 6;
 }
 void launch_cg_a(const SolveConst& c, int64_t rmax, cudaStream_t st) {
   SK_DISPATCH_S(c.s, cg_a(c, rmax, st));
@@ -1440,6 +1198,10 @@ void launch_spmm_plain(int s, const int32_t* rp, const int32_t* ci, const double
                        const double* x, double* y, int64_t n, cudaStream_t st) {
   SK_DISPATCH_S(s, spmm_plain(rp, ci, val, x, y, n, st));
   g_launches += 1;
+}
+void launch_export_block(int s, const double* blk, const double* nfac, int64_t b, double* out,
+                         int64_t n, cudaStream_t st) {
+  SK_DISPATCH_S(s, export_block(blk, nfac, b, out, n, st));
 }
 
 __global__ void k_block_to_colmajor(const double* blk, double* out, int64_t n, int s) {

@@ -9,9 +9,12 @@ int launch_count();
 void launch_count_reset();
 void launch_init(const SolveConst& c, const double* dc1, const double* dc2, cudaStream_t st);
 void launch_spmm(const SolveConst& c, cudaStream_t st);
-void launch_gram_lanczos(const SolveConst& c, cudaStream_t st);
+void launch_lanczos_gram(const SolveConst& c, cudaStream_t st);
+void launch_lanczos_update(const SolveConst& c, int64_t kmax_blocks, cudaStream_t st);
 void launch_rare(const SolveConst& c, int64_t kmax_blocks, cudaStream_t st);
-void launch_pass2(const SolveConst& c, cudaStream_t st);
+void launch_arnoldi_ext(const SolveConst& c, int64_t kmax_blocks, cudaStream_t st);
+void launch_export_block(int s, const double* blk, const double* nfac, int64_t b, double* out,
+                         int64_t n, cudaStream_t st);
 void launch_cg_a(const SolveConst& c, int64_t rmax, cudaStream_t st);
 void launch_cg_b(const SolveConst& c, int64_t rmax, cudaStream_t st);
 void launch_spmm_plain(int s, const int32_t* rp, const int32_t* ci, const double* val,

@@ -5,7 +5,7 @@ reference-order mode on short runs (north-star tolerance)."""
 import numpy as np
 import pytest
 
-from tests.helpers import bits_equal, max_rel, to_sk
+from helpers import bits_equal, max_rel, to_sk
 
 pytestmark = pytest.mark.gpu
 
