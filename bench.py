@@ -1,0 +1,310 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 factorized-Krylov hot path (driver contract).
+
+Workload (default --config 5 = BASELINE.json configs[4], the config the metric's
+1/2/4/8-GPU figures are quoted on and the largest single-GPU configuration):
+factorized CG for AX + XB = C1 C2^T with A = B = 5-point 2D Laplacian on a
+4096 x 4096 grid (n = m = 16,777,216), C1, C2 seeded N(0,1) 16.7M x 2 blocks,
+200 fixed iterations (time-to-1e-8 needs ~15k iterations and ~8 TB of basis).
+One step = one full solve (init + 200 iterations) from HBM-resident inputs.
+
+Timing: W untimed warm-up solves, then K solves timed with CUDA events inside
+the library (whole solve, on its stream); inputs (CSR 1.07 GB + 108 GB of
+bases per solve) are far larger than the 126 MB L2. value = iterations / s
+(max over ranks). e2e = the same metric through sk_factorized_cg with host
+buffers (host validation + transposition + H2D + solve + D2H of history and core).
+
+--impl reference: the reference's algorithm on the host cores (the reference
+itself cannot be built here -- Eigen3/GTest/vendor headers absent -- so its C
+restatement in oracle/, reference-order mode, parallel SpMM), on a bounded
+sample (first --cpu-iters iterations) of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "Krylov iters/sec (factorized CG; also time-to-tolerance and HBM GB/s vs peak)"
+UNIT = "iter/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--config", type=int, default=5)
+    ap.add_argument("--cpu-iters", type=int, default=2)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=1)
+    return ap.parse_args()
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.out = ""
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.out, _ = self.proc.communicate(timeout=5)
+        except Exception:
+            self.proc.kill()
+            self.out = ""
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.out.strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                smax = float(f[2])
+            except ValueError:
+                continue
+            for name, val in zip(names, f[5:9]):
+                if val.lower() == "active":
+                    reasons.add(name)
+        load = [x for x in sm if smax and x > 0.5 * smax] or sm
+        return {"sm_mhz": statistics.median(load) if load else None, "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def dist_setup(args):
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    dist = None
+    if world > 1:
+        import torch
+        import torch.distributed as tdist
+        torch.cuda.set_device(local)
+        tdist.init_process_group("nccl")
+        dist = tdist
+    return rank, world, local, dist
+
+
+def max_over_ranks(x: float, dist, local: int) -> float:
+    if dist is None:
+        return x
+    import torch
+    t = torch.tensor([x], dtype=torch.float64, device=f"cuda:{local}")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier_sync(dist, local):
+    try:
+        import torch
+        torch.cuda.synchronize(local)
+    except Exception:
+        pass
+    if dist is not None:
+        dist.barrier()
+
+
+def cpu_reference(cfg_idx: int, iters: int, threads: int):
+    """The reference algorithm on host cores (oracle reference-order restatement)."""
+    from oracle import pyoracle as po
+    import numpy as np
+    if cfg_idx == 5:
+        a = po.laplacian_2d(4096)
+        c1, c2 = po.random_rhs(1 << 24, 2, 1234), po.random_rhs(1 << 24, 2, 1235)
+        method, b = po.CG, a
+    elif cfg_idx == 1:
+        a = po.laplacian_2d(64)
+        c1 = po.random_rhs(4096, 1, 1234); c1 /= np.linalg.norm(c1)
+        c2 = po.random_rhs(4096, 1, 1235); c2 /= np.linalg.norm(c2)
+        method, b = po.CG, a
+    elif cfg_idx == 3:
+        a = po.laplacian_2d(1024)
+        c1, c2, b, method = po.random_rhs(1 << 20, 1, 1234), None, None, po.CG_LYAPUNOV
+    else:
+        raise SystemExit(f"no CPU sample defined for config {cfg_idx}")
+    po.set_parallel(threads > 1, threads)
+    sol = po.solve(method, a, b, c1, c2, po.Config(eps_tol=1e-8, max_iter=iters), po.REFERENCE_ORDER)
+    po.set_parallel(False, 1)
+    return sol.n_iterations, sol.total_time_s
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    threads = os.cpu_count() or 1
+    for _ in range(args.warmup):
+        cpu_reference(args.config, args.cpu_iters, threads)
+    its, secs = 0, 0.0
+    for _ in range(args.steps):
+        i, t = cpu_reference(args.config, args.cpu_iters, threads)
+        its += i
+        secs += t
+    v = its / secs
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * secs / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": {"workload": f"C{args.config}", "sample": f"first {args.cpu_iters} iterations"},
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": "port",
+                         "sample": f"config C{args.config}, first {args.cpu_iters} iterations per step, "
+                                   f"oracle reference-order restatement (reference unbuildable: Eigen3/GTest absent), "
+                                   f"SpMM threaded over {threads} host threads as in parallel.cpp"},
+        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    rank, world, local, dist = dist_setup(args)
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    import numpy as np
+    import paper_2605_28274_b200 as sk
+    from paper_2605_28274_b200 import build as skbuild
+    from paper_2605_28274_b200.problems import baseline_config
+    skbuild.build()
+    if sk.device_count() < 1:
+        raise SystemExit("bench: no CUDA device")
+    cfg = baseline_config(args.config)
+    scfg = sk.SolverConfig(eps_tol=cfg.eps_tol, max_iter=cfg.max_iter)
+    gpu = sk.GpuOptions(device=local, profile=True)
+    prob = sk.ResidentProblem(cfg.method, cfg.a, cfg.b, cfg.c1, cfg.c2, gpu=gpu)
+
+    for _ in range(args.warmup):
+        sol = prob.solve(scfg)
+        sol.free()
+
+    sampler = ClockSampler(local)
+    barrier_sync(dist, local)
+    sampler.start()
+    wall0 = time.perf_counter()
+    dev_s, iters, launches = 0.0, 0, 0
+    classes = {}
+    hist = None
+    for _ in range(args.steps):
+        sol = prob.solve(scfg)
+        dev_s += sol.stats["device_time_s"]
+        iters += sol.history.iterations()
+        launches += sol.stats["kernel_launches"]
+        for name, c in sol.stats["classes"].items():
+            acc = classes.setdefault(name, {"time_s": 0.0, "bytes": 0.0, "launches": 0})
+            acc["time_s"] += c["time_s"]
+            acc["bytes"] += c["bytes"]
+            acc["launches"] += c["launches"]
+        hist = sol.history
+        status = sol.status
+        sol.free()
+    barrier_sync(dist, local)
+    wall = time.perf_counter() - wall0
+    clocks = sampler.stop()
+    prob.free()
+
+    dev_max = max_over_ranks(dev_s, dist, local)
+    total_iters = iters * world
+    value = total_iters / dev_max
+    peak, peak_src = peaks()
+    dom = max(classes.items(), key=lambda kv: kv[1]["time_s"])
+    achieved = dom[1]["bytes"] / dom[1]["time_s"] / 1e9 if dom[1]["time_s"] > 0 else 0.0
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tp):
+        traffic = json.load(open(tp)).get(f"C{args.config}", {}).get(dom[0])
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 * dev_max / args.steps, "higher_is_better": True,
+        "scaling": "weak" if world > 1 else "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded random_rhs N(0,1) blocks, stencil operators; BASELINE.json configs)",
+        "config": {"workload": f"{cfg.name}: {cfg.description}", "n": cfg.a.n_rows,
+                   "s": int(cfg.c1.shape[1]), "iterations_per_step": iters // max(args.steps, 1),
+                   "final_rel_residual": hist.final_rel_residual() if hist else None,
+                   "status": status, "parallelism": f"replicas x{world}" if world > 1 else "1 GPU",
+                   "l2": "inputs larger than L2 (CSR 1.07 GB + 108 GB bases per solve at C5)",
+                   "wall_s_timed_region": wall},
+        "roofline": {"bound": "hbm", "kernel": dom[0], "achieved": achieved, "peak": peak,
+                     "peak_source": peak_src, "unit": "GB/s", "frac": achieved / peak,
+                     "traffic": traffic,
+                     "classes": {k: {"GBps": (v["bytes"] / v["time_s"] / 1e9) if v["time_s"] > 0 else None,
+                                     "share": v["time_s"] / max(dev_s, 1e-30), "launches": v["launches"]}
+                                 for k, v in classes.items() if v["launches"]}},
+        "clocks": clocks,
+        "gpu_launches": launches,
+    }
+
+    if rank == 0 and not args.no_e2e:
+        e2e_its, e2e_s, h2d, d2h = 0, 0.0, 0, 0
+        for _ in range(args.e2e_steps):
+            t0 = time.perf_counter()
+            if cfg.method == "cg":
+                sol = sk.factorized_cg(cfg.a, cfg.b, cfg.c1, cfg.c2, scfg, sk.GpuOptions(device=local))
+            elif cfg.method == "cg_lyapunov":
+                sol = sk.factorized_cg_lyapunov(cfg.a, cfg.c1, scfg, sk.GpuOptions(device=local))
+            else:
+                sol = sk.factorized_bicgstab(cfg.a, cfg.b, cfg.c1, cfg.c2, scfg, sk.GpuOptions(device=local))
+            core = sol.core  # D2H of the result core (V, W stay in HBM until requested)
+            e2e_s += time.perf_counter() - t0
+            e2e_its += sol.history.iterations()
+            h2d += sol.stats["h2d_bytes"]
+            d2h += sol.stats["d2h_bytes"] + core.nbytes
+            sol.free()
+        line["e2e"] = {"value": e2e_its / e2e_s, "unit": UNIT,
+                       "h2d_bytes_per_step": h2d // args.e2e_steps,
+                       "d2h_bytes_per_step": d2h // args.e2e_steps,
+                       "note": "includes host CSR validation/symmetry checks/transposition"}
+
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            its, secs = cpu_reference(args.config, args.cpu_iters, 1)
+            line["cpu_baseline"] = {
+                "value": its / secs, "unit": UNIT, "cores": 1, "kind": "port",
+                "sample": f"C{args.config}, first {its} iterations, serial oracle reference-order "
+                          f"restatement (-O3, no -march, as proj/CMakeLists.txt), solve window only"}
+        except SystemExit as e:
+            line["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": 1, "kind": "port", "sample": str(e)}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

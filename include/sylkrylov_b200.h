@@ -134,6 +134,16 @@ int32_t sk_device_count(void);
  * y = A^T x (spmm_transpose, via the transposed CSR) on the device. */
 sk_status sk_spmm(const sk_csr* a, const double* x, int64_t s, int32_t transpose, double* y);
 
+/* Problem generators (problems.cpp:10-96 restated, plus the 2D convection-
+ * diffusion sibling): kind 0 = laplacian_2d, 1 = convection_diffusion_2d,
+ * 2 = convection_diffusion_3d (wind = convection vector w; Peclet Pe with a
+ * unit wind d is w = Pe*d). Caller allocates n+1 / nnz / nnz entries. */
+int64_t sk_gen_stencil_nnz(int32_t kind, int64_t grid);
+sk_status sk_gen_stencil(int32_t kind, int64_t grid, const double* wind, int64_t* row_ptr,
+                         int64_t* col_idx, double* values);
+/* random_rhs: rows x s column-major, std::mt19937_64 + Box-Muller (bitwise the reference's). */
+sk_status sk_gen_random_rhs(int64_t rows, int64_t s, uint64_t seed, double* out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -87,7 +87,7 @@ class _Stats(C.Structure):
                 ("paths", C.c_int64 * 4)]
 
 
-KERNEL_CLASSES = ["spmm", "gram", "rare_path", "write_block", "core_a", "core_b",
+KERNEL_CLASSES = ["spmm", "gram", "rare_path", "update", "core_a", "core_b",
                   "arnoldi_update", "dense_image", "other"]
 
 _lib = None

@@ -26,6 +26,7 @@ def units():
     u = [("sk_kernels.cu", f"sk_kernels_s{s}.o", [f"-DSK_INST_S={s}"]) for s in S_VALUES]
     u.append(("sk_kernels.cu", "sk_kernels_common.o", ["-DSK_INST_COMMON"]))
     u.append(("sk_driver.cu", "sk_driver.o", []))
+    u.append(("sk_problems.cpp", "sk_problems.o", []))
     return u
 
 
@@ -41,7 +42,11 @@ def needs_build() -> bool:
 
 def _compile(unit, verbose):
     src, obj, defs = unit
-    cmd = [NVCC, *FLAGS, *defs, "-c", os.path.join(CSRC, src), "-o", os.path.join(CSRC, obj)]
+    if src.endswith(".cpp"):
+        cmd = ["g++", "-O3", "-std=c++17", "-fPIC", "-Wall", "-ffp-contract=off", "-pthread", *defs,
+               "-c", os.path.join(CSRC, src), "-o", os.path.join(CSRC, obj)]
+    else:
+        cmd = [NVCC, *FLAGS, *defs, "-c", os.path.join(CSRC, src), "-o", os.path.join(CSRC, obj)]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
     r = subprocess.run(cmd, capture_output=True, text=True)
@@ -60,7 +65,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
         for lg in logs:
             sys.stderr.write(lg)
     objs = [os.path.join(CSRC, u[1]) for u in us]
-    subprocess.check_call([NVCC, "-shared", *ARCH, *objs, "-o", LIB + ".tmp", "-lcudart"])
+    subprocess.check_call([NVCC, "-shared", *ARCH, *objs, "-o", LIB + ".tmp", "-lcudart",
+                           "-Xcompiler", "-pthread"])
     os.replace(LIB + ".tmp", LIB)
     return LIB
 

@@ -84,9 +84,14 @@ HostCsr transpose(const sk_csr* a) {
   return t;
 }
 
+bool is_symmetric_with(const sk_csr* a, const HostCsr& at, double tol);
 bool is_symmetric(const sk_csr* a, double tol) {
   if (a->n_rows != a->n_cols) return false;
-  HostCsr at = transpose(a);
+  return is_symmetric_with(a, transpose(a), tol);
+}
+// ||A - A^T||_F <= tol ||A||_F given the transpose (sparse_matrix.cpp:109-132)
+bool is_symmetric_with(const sk_csr* a, const HostCsr& at, double tol) {
+  if (a->n_rows != a->n_cols) return false;
   double diff2 = 0.0, fro = 0.0;
   for (int64_t k = 0; k < a->nnz; ++k) fro += a->values[k] * a->values[k];
   for (int64_t i = 0; i < a->n_rows; ++i) {
@@ -111,6 +116,22 @@ bool is_symmetric(const sk_csr* a, double tol) {
 // ---------------------------------------------------------------------------
 // Device CSR (int32 indices: every n, nnz of the configs is < 2^31)
 // ---------------------------------------------------------------------------
+// bitwise equality of a CSR and a host CSR (used to share device copies)
+bool same_csr(const sk_csr* a, const HostCsr& b) {
+  if (a->n_rows != b.n_rows || a->n_cols != b.n_cols || a->nnz != (int64_t)b.val.size()) return false;
+  return std::memcmp(a->row_ptr, b.rp.data(), sizeof(int64_t) * (a->n_rows + 1)) == 0 &&
+         std::memcmp(a->col_idx, b.ci.data(), sizeof(int64_t) * a->nnz) == 0 &&
+         std::memcmp(a->values, b.val.data(), sizeof(double) * a->nnz) == 0;
+}
+bool same_csr(const sk_csr* a, const sk_csr* b) {
+  if (a == b) return true;
+  if (a->n_rows != b->n_rows || a->n_cols != b->n_cols || a->nnz != b->nnz) return false;
+  if (a->row_ptr == b->row_ptr && a->col_idx == b->col_idx && a->values == b->values) return true;
+  return std::memcmp(a->row_ptr, b->row_ptr, sizeof(int64_t) * (a->n_rows + 1)) == 0 &&
+         std::memcmp(a->col_idx, b->col_idx, sizeof(int64_t) * a->nnz) == 0 &&
+         std::memcmp(a->values, b->values, sizeof(double) * a->nnz) == 0;
+}
+
 struct DevCsr {
   int64_t n = 0, nnz = 0;
   int32_t* rp = nullptr;
@@ -155,6 +176,7 @@ struct sk_problem {
   int profile = 0;
   int64_t capacity_bytes = 0;
   DevCsr op[2];  // side 0: A (V basis), side 1: B^T (W basis)
+  bool op_shared = false;  // B^T bitwise equal to A: one device copy serves both sides
   double* c1 = nullptr;
   double* c2 = nullptr;
   cudaStream_t stream = nullptr;
@@ -653,17 +675,24 @@ sk_problem* create_problem(int32_t method, const sk_csr* a, const sk_csr* b, con
                            const double* c2, int64_t s, const sk_gpu_options* gpu) {
   validate_csr(a, "A");
   const bool lyap = method == SK_METHOD_CG_LYAPUNOV;
+  HostCsr bt;  // B^T: the W basis applies it (block_krylov.cpp:54-56)
   if (lyap) {
     if (a->n_rows != a->n_cols) throw SkError(SK_ERR_DIMENSION, "factorized_cg_lyapunov: A must be square");
     if (!is_symmetric(a, 1e-12)) throw SkError(SK_ERR_INVALID_MATRIX, "factorized_cg_lyapunov: A is not symmetric");
   } else {
-    validate_csr(b, "B");
+    const bool ab_same = same_csr(a, b);
+    if (!ab_same) validate_csr(b, "B");
     if (a->n_rows != a->n_cols || b->n_rows != b->n_cols)
       throw SkError(SK_ERR_DIMENSION, "solver: A and B must be square");
     if (s < 1) throw SkError(SK_ERR_DIMENSION, "solver: C1 and C2 must have the same positive column count");
+    bt = transpose(b);
     if (method == SK_METHOD_CG) {
-      if (!is_symmetric(a, 1e-12)) throw SkError(SK_ERR_INVALID_MATRIX, "factorized_cg: A is not symmetric");
-      if (!is_symmetric(b, 1e-12)) throw SkError(SK_ERR_INVALID_MATRIX, "factorized_cg: B is not symmetric");
+      if (ab_same) {
+        if (!is_symmetric_with(a, bt, 1e-12)) throw SkError(SK_ERR_INVALID_MATRIX, "factorized_cg: A is not symmetric");
+      } else if (!is_symmetric(a, 1e-12)) {
+        throw SkError(SK_ERR_INVALID_MATRIX, "factorized_cg: A is not symmetric");
+      }
+      if (!is_symmetric_with(b, bt, 1e-12)) throw SkError(SK_ERR_INVALID_MATRIX, "factorized_cg: B is not symmetric");
     }
   }
   if (s < 1 || s > a->n_rows) throw SkError(SK_ERR_DIMENSION, "basis init: block size must be in [1, n]");
@@ -681,12 +710,24 @@ sk_problem* create_problem(int32_t method, const sk_csr* a, const sk_csr* b, con
   p->profile = gpu ? gpu->profile : 0;
   p->capacity_bytes = gpu ? gpu->capacity_bytes : 0;
   CK(cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking));
+  {
+    // keep freed basis memory mapped in the pool across solves (no re-mapping per solve)
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t thr = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+  }
   auto t0 = std::chrono::steady_clock::now();
   p->h2d_bytes += upload_csr(p->op[0], a->n_rows, a->nnz, a->row_ptr, a->col_idx, a->values, p->stream);
   if (!lyap) {
-    HostCsr bt = transpose(b);  // W basis applies B^T (block_krylov.cpp:54-56)
-    p->h2d_bytes += upload_csr(p->op[1], bt.n_rows, (int64_t)bt.val.size(), bt.rp.data(),
-                               bt.ci.data(), bt.val.data(), p->stream);
+    if (same_csr(a, bt)) {
+      p->op[1] = p->op[0];  // e.g. A = B symmetric: B^T == A bitwise
+      p->op_shared = true;
+    } else {
+      p->h2d_bytes += upload_csr(p->op[1], bt.n_rows, (int64_t)bt.val.size(), bt.rp.data(),
+                                 bt.ci.data(), bt.val.data(), p->stream);
+    }
   }
   CK(cudaMalloc(&p->c1, sizeof(double) * p->n * s));
   CK(cudaMemcpyAsync(p->c1, c1, sizeof(double) * p->n * s, cudaMemcpyHostToDevice, p->stream));
@@ -705,7 +746,7 @@ void destroy_problem(sk_problem* p) {
   if (!p) return;
   cudaSetDevice(p->device);
   free_csr(p->op[0]);
-  free_csr(p->op[1]);
+  if (!p->op_shared) free_csr(p->op[1]);
   cudaFree(p->c1);
   cudaFree(p->c2);
   // the stream is shared with solutions; leave it to the process

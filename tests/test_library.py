@@ -1,0 +1,78 @@
+"""CPU-side checks of the product library: it loads, exports every C-ABI symbol
+include/sylkrylov_b200.h declares, its host-side generators equal the oracle's
+bitwise, and the solver fails loudly (no CPU fallback) without a CUDA device."""
+import os
+import re
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def skl():
+    from paper_2605_28274_b200 import build
+    build.build()
+    import paper_2605_28274_b200 as sk
+    sk.lib()
+    return sk
+
+
+def header_symbols():
+    src = open(os.path.join(ROOT, "include", "sylkrylov_b200.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(sk_[A-Za-z0-9_]+)\s*\(", src)))
+
+
+def test_exports_every_header_symbol(skl):
+    syms = header_symbols()
+    assert len(syms) >= 25
+    missing = [s for s in syms if not hasattr(skl.lib(), s)]
+    assert not missing, missing
+
+
+def test_built_for_sm100a():
+    lib = os.path.join(ROOT, "paper_2605_28274_b200", "libsk_b200.so")
+    out = os.popen(f"/usr/local/cuda/bin/cuobjdump --list-elf {lib} 2>/dev/null").read()
+    assert "sm_100a" in out
+
+
+@pytest.mark.parametrize("grid", [2, 5, 17])
+def test_generators_match_oracle(skl, grid):
+    from oracle import pyoracle as po
+    from paper_2605_28274_b200 import problems as pr
+    a, b = pr.laplacian_2d(grid), po.laplacian_2d(grid)
+    assert np.array_equal(a.row_ptr, b.row_ptr) and np.array_equal(a.col_idx, b.col_idx)
+    assert np.array_equal(a.values, b.values)
+    a, b = pr.convection_diffusion_2d(grid, (10.0, -10.0)), po.convection_diffusion_2d(grid, (10.0, -10.0))
+    assert np.array_equal(a.col_idx, b.col_idx) and np.array_equal(a.values, b.values)
+    if grid <= 5:
+        a, b = pr.convection_diffusion_3d(grid, (5.0, 2.5, 1.25)), po.convection_diffusion_3d(grid, (5.0, 2.5, 1.25))
+        assert np.array_equal(a.row_ptr, b.row_ptr) and np.array_equal(a.values, b.values)
+    assert np.array_equal(pr.random_rhs(101, 3, 77), po.random_rhs(101, 3, 77))
+
+
+def test_large_laplacian_parallel_fill(skl):
+    from oracle import pyoracle as po
+    from paper_2605_28274_b200 import problems as pr
+    a, b = pr.laplacian_2d(700), po.laplacian_2d(700)
+    assert np.array_equal(a.row_ptr, b.row_ptr) and np.array_equal(a.col_idx, b.col_idx)
+
+
+def test_no_cpu_fallback(skl):
+    if skl.device_count() > 0:
+        pytest.skip("a CUDA device is present")
+    a = skl.SparseMatrix.identity(4)
+    with pytest.raises(skl.CudaError):
+        skl.factorized_cg(a, a, np.ones((4, 1)), np.ones((4, 1)))
+
+
+def test_input_validation_before_device(skl):
+    """Reference error taxonomy (errors.hpp) is raised by host validation."""
+    bad = skl.SparseMatrix(2, 2, np.array([0, 1, 2]), np.array([0, 2]), np.array([1.0, 1.0]))
+    with pytest.raises(skl.InvalidMatrixError):
+        skl.factorized_cg(bad, bad, np.ones((2, 1)), np.ones((2, 1)))
+    a = skl.SparseMatrix.identity(3)
+    with pytest.raises(skl.DimensionError):
+        skl.factorized_cg(a, a, np.ones((4, 1)), np.ones((3, 1)))
