@@ -795,7 +795,9 @@ struct sko_basis {
     int transpose, arnoldi, full_reorth, mode;
     double tol;
     int64_t n, s, blocks, cap;
-    double* v; /* n x cap*s, column-major, block b = columns [b*s, b*s+s) */
+    double* v; /* n x cap*s, column-major, block b = columns [b*s, b*s+s) (orthonormal V) */
+    double* u;  /* reproducible mode: raw blocks U_b with V_b = U_b N_b^{-1} */
+    double* nf; /* reproducible mode: N_b (s x s, column-major) per block */
     double** hcol;
     int64_t* hrows;
     int64_t steps, hcap;
@@ -805,14 +807,26 @@ struct sko_basis {
 };
 
 static double* blk(const sko_basis* b, int64_t j) { return b->v + (size_t)(j * b->s * b->n); }
+static double* ublk(const sko_basis* b, int64_t j) { return b->u + (size_t)(j * b->s * b->n); }
+static double* nfb(const sko_basis* b, int64_t j) { return b->nf + (size_t)(j * b->s * b->s); }
 
-static void basis_append(sko_basis* b, const double* q) {
+/* q: orthonormal block; u/N: its raw form and factor (reproducible mode only) */
+static void basis_append(sko_basis* b, const double* q, const double* u, const double* N) {
     if (b->blocks == b->cap) {
         b->cap = b->cap ? 2 * b->cap : 8;
         b->v = (double*)realloc(b->v, sizeof(double) * (size_t)(b->cap * b->s * b->n));
         if (!b->v) abort();
+        if (b->mode == SKO_REPRODUCIBLE) {
+            b->u = (double*)realloc(b->u, sizeof(double) * (size_t)(b->cap * b->s * b->n));
+            b->nf = (double*)realloc(b->nf, sizeof(double) * (size_t)(b->cap * b->s * b->s));
+            if (!b->u || !b->nf) abort();
+        }
     }
     memcpy(blk(b, b->blocks), q, sizeof(double) * (size_t)(b->s * b->n));
+    if (b->mode == SKO_REPRODUCIBLE) {
+        memcpy(ublk(b, b->blocks), u, sizeof(double) * (size_t)(b->s * b->n));
+        memcpy(nfb(b, b->blocks), N, sizeof(double) * (size_t)(b->s * b->s));
+    }
     b->blocks++;
 }
 static void basis_push_h(sko_basis* b, double* col, int64_t rows) {
@@ -868,16 +882,57 @@ static void apply_norm(const sko_basis* b, const double* w, const double* N, dou
         }
 }
 
+/* c = N^{-T} G (forward substitution, N^T lower): c(t,u) = (G(t,u) - sum_{r<t} N(r,t) c(r,u)) / N(t,t) */
+static void tri_ntinv(const double* N, const double* G, int64_t s, double* c) {
+    double dinv[64];
+    for (int64_t t = 0; t < s; ++t) dinv[t] = 1.0 / N[t * s + t];
+    for (int64_t u = 0; u < s; ++u)
+        for (int64_t t = 0; t < s; ++t) {
+            double acc = G[u * s + t];
+            for (int64_t r = 0; r < t; ++r) acc = acc - N[t * s + r] * c[u * s + r];
+            c[u * s + t] = acc * dinv[t];
+        }
+}
+/* M = N^{-1} c (backward substitution): M(t,u) = (c(t,u) - sum_{r>t} N(t,r) M(r,u)) / N(t,t) */
+static void tri_ninv(const double* N, const double* c, int64_t s, double* M) {
+    double dinv[64];
+    for (int64_t t = 0; t < s; ++t) dinv[t] = 1.0 / N[t * s + t];
+    for (int64_t u = 0; u < s; ++u)
+        for (int64_t t = s - 1; t >= 0; --t) {
+            double acc = c[u * s + t];
+            for (int64_t r = t + 1; r < s; ++r) acc = acc - N[r * s + t] * M[u * s + r];
+            M[u * s + t] = acc * dinv[t];
+        }
+}
+/* reproducible CGS pass against raw blocks [b0,b1): c_b = N_b^{-T} (U_b^T x) (R1);
+ * then x <- x - sum_b U_b (N_b^{-1} c_b) */
+static void cgs_raw(const sko_basis* b, int64_t b0, int64_t b1, double* x, double* c_out, int update) {
+    const int64_t s = b->s, ss = s * s;
+    double G[64 * 64], M[64 * 64];
+    double* Ms = (double*)xcalloc((size_t)((b1 - b0 + 1) * ss), sizeof(double));
+    for (int64_t jb = b0; jb < b1; ++jb) {
+        gram(b, ublk(b, jb), x, G);
+        tri_ntinv(nfb(b, jb), G, s, c_out + jb * ss);
+        tri_ninv(nfb(b, jb), c_out + jb * ss, s, M);
+        memcpy(Ms + (jb - b0) * ss, M, sizeof(double) * (size_t)ss);
+    }
+    if (update)
+        for (int64_t jb = b0; jb < b1; ++jb) sub_vc(b, ublk(b, jb), Ms + (jb - b0) * ss, x);
+    free(Ms);
+}
+
 /* Normalisation of a materialised candidate wx under the reproducible contract:
  * direct R1 Gram -> Cholesky -> sigma extremes; Householder (with R1 dots) when
  * the Gram is not positive definite or sigma_min < 1e-6 sigma_max. */
 typedef struct {
     double R[64 * 64];
+    double N[64 * 64]; /* normalisation factor stored with the raw block */
     double smax, smin;
     int householder;
 } norm_result;
 
-static void norm_direct(const sko_basis* b, const double* wx, double* Q, norm_result* nr) {
+/* Q: orthonormal block; U (optional): the raw block stored by the device */
+static void norm_direct(const sko_basis* b, const double* wx, double* Q, norm_result* nr, double* U) {
     const int64_t s = b->s, n = b->n;
     double G[64 * 64];
     gram(b, wx, wx, G);
@@ -887,16 +942,18 @@ static void norm_direct(const sko_basis* b, const double* wx, double* Q, norm_re
         if (nr->smin < HH_RATIO * nr->smax) ok = 0;
     }
     if (ok) {
+        if (U) memcpy(U, wx, sizeof(double) * (size_t)(n * s));
+        memcpy(nr->N, nr->R, sizeof(double) * (size_t)(s * s));
         apply_norm(b, wx, nr->R, Q);
         nr->householder = 0;
     } else {
         double* qh = (double*)xcalloc((size_t)(n * s), sizeof(double));
         householder_qr(wx, n, s, r1_dot, qh, nr->R);
         jacobi_extremes(nr->R, s, s, &nr->smax, &nr->smin);
-        double I[64 * 64];
-        memset(I, 0, sizeof I);
-        for (int64_t u = 0; u < s; ++u) I[u * s + u] = 1.0;
-        apply_norm(b, qh, I, Q); /* the device reads Q_h through an identity factor */
+        memset(nr->N, 0, sizeof nr->N);
+        for (int64_t u = 0; u < s; ++u) nr->N[u * s + u] = 1.0;
+        if (U) memcpy(U, qh, sizeof(double) * (size_t)(n * s));
+        apply_norm(b, qh, nr->N, Q); /* the device reads Q_h through an identity factor */
         free(qh);
         nr->householder = 1;
     }
@@ -925,7 +982,8 @@ int sko_basis_init(const sko_csr* op, const double* start, int64_t s, int arnold
     }
     const int64_t n = b->n;
     double* q = (double*)xcalloc((size_t)(n * s), sizeof(double));
-    double R[64 * 64];
+    double* ub = (double*)xcalloc((size_t)(n * s), sizeof(double));
+    double R[64 * 64], N[64 * 64];
     double smax, smin;
     if (mode == SKO_REFERENCE_ORDER) {
         householder_qr(start, n, s, seq_dot, q, R);
@@ -933,20 +991,23 @@ int sko_basis_init(const sko_csr* op, const double* start, int64_t s, int arnold
     } else {
         norm_result nr;
         memset(&nr, 0, sizeof nr);
-        norm_direct(b, start, q, &nr);
+        norm_direct(b, start, q, &nr, ub);
         memcpy(R, nr.R, sizeof(double) * (size_t)(s * s));
+        memcpy(N, nr.N, sizeof(double) * (size_t)(s * s));
         smax = nr.smax;
         smin = nr.smin;
         b->paths[nr.householder ? PATH_HOUSEHOLDER : PATH_DIRECT]++;
     }
     if (smin < 1e-12 * smax || smax == 0.0) {
         free(q);
+        free(ub);
         if (b->has_opT) sko_csr_free(&b->opT);
         free(b);
         return set_err("basis init: start block is numerically rank deficient"), SKO_ERR_RANK_DEFICIENT;
     }
-    basis_append(b, q);
+    basis_append(b, q, ub, N);
     free(q);
+    free(ub);
     if (r_out) memcpy(r_out, R, sizeof(double) * (size_t)(s * s));
     *out = b;
     return SKO_OK;
@@ -959,10 +1020,19 @@ int sko_basis_try_extend(sko_basis* b) {
     const int64_t n = b->n, s = b->s, k = b->blocks, ss = s * s;
     const int64_t first = b->arnoldi ? 0 : (k - 2 > 0 ? k - 2 : 0);
     double* w = (double*)xcalloc((size_t)(n * s), sizeof(double));
-    basis_apply(b, blk(b, k - 1), w);
+    if (b->mode == SKO_REFERENCE_ORDER) {
+        basis_apply(b, blk(b, k - 1), w);
+    } else {
+        /* w = (op U_{k-1}) N_{k-1}^{-1}: raw SpMM, then one row normalisation */
+        double* wr = (double*)xcalloc((size_t)(n * s), sizeof(double));
+        basis_apply(b, ublk(b, k - 1), wr);
+        apply_norm(b, wr, nfb(b, k - 1), w);
+        free(wr);
+    }
     double* hcoef = (double*)xcalloc((size_t)(k * ss), sizeof(double)); /* block jb at jb*ss */
     double* q = (double*)xcalloc((size_t)(n * s), sizeof(double));
-    double R[64 * 64];
+    double* uk = (double*)xcalloc((size_t)(n * s), sizeof(double));
+    double R[64 * 64], NK[64 * 64];
     double smax = 0, smin = 0;
     int path = PATH_DIRECT, hh = 0;
 
@@ -989,39 +1059,25 @@ int sko_basis_try_extend(sko_basis* b) {
         jacobi_extremes(R, s, s, &smax, &smin);
         hh = 1;
     } else {
-        /* reproducible contract: CGS pass(es), materialised candidate, direct CholQR */
+        /* reproducible contract: CGS pass(es) on the raw blocks, direct CholQR */
         double* cc = (double*)xcalloc((size_t)(k * ss), sizeof(double));
-        double* base = w;
-        double* w1 = NULL;
-        int64_t c0 = first;
-        for (int64_t jb = first; jb < k; ++jb) gram(b, blk(b, jb), w, hcoef + jb * ss);
+        cgs_raw(b, first, k, w, hcoef, 1); /* w <- w - V_J c_J */
         if (b->arnoldi || b->full_reorth) {
             /* second CGS pass (Arnoldi: recorded into H; full re-orth: not recorded) */
-            w1 = (double*)xcalloc((size_t)(n * s), sizeof(double));
-            memcpy(w1, w, sizeof(double) * (size_t)(n * s));
-            for (int64_t jb = first; jb < k; ++jb) sub_vc(b, blk(b, jb), hcoef + jb * ss, w1);
-            for (int64_t jb = 0; jb < k; ++jb) gram(b, blk(b, jb), w1, cc + jb * ss);
+            cgs_raw(b, 0, k, w, cc, 1);
             if (b->arnoldi)
                 for (int64_t e = 0; e < k * ss; ++e) hcoef[e] = hcoef[e] + cc[e];
-            base = w1;
-            c0 = 0;
-        } else {
-            for (int64_t jb = first; jb < k; ++jb)
-                memcpy(cc + jb * ss, hcoef + jb * ss, sizeof(double) * (size_t)ss);
         }
-        /* wx = base - sum_b V_b cc_b, kept in w for a possible clean-up pass */
-        if (base != w) memcpy(w, base, sizeof(double) * (size_t)(n * s));
-        for (int64_t jb = c0; jb < k; ++jb) sub_vc(b, blk(b, jb), cc + jb * ss, w);
         norm_result nr;
         memset(&nr, 0, sizeof nr);
-        norm_direct(b, w, q, &nr);
+        norm_direct(b, w, q, &nr, uk);
         memcpy(R, nr.R, sizeof(double) * (size_t)ss);
+        memcpy(NK, nr.N, sizeof(double) * (size_t)ss);
         smax = nr.smax;
         smin = nr.smin;
         path = nr.householder ? PATH_HOUSEHOLDER : PATH_DIRECT;
         hh = nr.householder;
         free(cc);
-        free(w1);
     }
     (void)hh;
     b->paths[b->mode == SKO_REPRODUCIBLE ? path : PATH_HOUSEHOLDER]++;
@@ -1049,12 +1105,12 @@ int sko_basis_try_extend(sko_basis* b) {
             jacobi_extremes(R, s, s, &smax, &smin);
         } else {
             double* d = (double*)xcalloc((size_t)(k * ss), sizeof(double));
-            for (int64_t jb = 0; jb < k; ++jb) gram(b, blk(b, jb), w, d + jb * ss);
-            for (int64_t jb = 0; jb < k; ++jb) sub_vc(b, blk(b, jb), d + jb * ss, w);
+            cgs_raw(b, 0, k, w, d, 1);
             norm_result nr;
             memset(&nr, 0, sizeof nr);
-            norm_direct(b, w, q, &nr);
+            norm_direct(b, w, q, &nr, uk);
             memcpy(R, nr.R, sizeof(double) * (size_t)ss);
+            memcpy(NK, nr.N, sizeof(double) * (size_t)ss);
             smax = nr.smax;
             smin = nr.smin;
             b->paths[PATH_CLEANUP]++;
@@ -1086,12 +1142,13 @@ int sko_basis_try_extend(sko_basis* b) {
         }
         basis_push_h(b, col, rows);
         b->hfro2 = b->hfro2 + coeff2 + r2;
-        basis_append(b, q);
+        basis_append(b, q, uk, NK);
         rc = 0;
     }
     free(w);
     free(hcoef);
     free(q);
+    free(uk);
     return rc;
 }
 
@@ -1105,6 +1162,8 @@ void sko_basis_path_counts(const sko_basis* b, int64_t* out4) { memcpy(out4, b->
 void sko_basis_free(sko_basis* b) {
     if (!b) return;
     free(b->v);
+    free(b->u);
+    free(b->nf);
     for (int64_t e = 0; e < b->steps; ++e) free(b->hcol[e]);
     free(b->hcol);
     free(b->hrows);

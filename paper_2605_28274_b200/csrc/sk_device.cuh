@@ -80,10 +80,19 @@ struct SideConst {
   double* nfac;              // [cap_blocks][s*s + s] normalisation factor N_b and 1/diag
   double* coef;              // [cap_blocks][s*s] CGS coefficients (pass 1)
   double* coef2;             // [cap_blocks][s*s] second-pass coefficients
+  double* mcoef;             // [cap_blocks][s*s] M_b = N_b^{-1} c_b (pass 1)
+  double* mcoef2;            // [cap_blocks][s*s] second-pass M_b
   double* part;              // R1 CTA partials
   unsigned int* counter;     // last-CTA counters (several slots)
   int64_t ncta;              // CTAs covering n rows (kRowsPerCta each)
   int64_t nseg;              // R1 segments
+  // matrix-free stencil form of the operator (0: use the CSR). Detected on the
+  // host from the CSR itself: rows are exactly the Dirichlet-truncated grid
+  // stencil with one constant value per offset, in CSR (ascending) order.
+  int32_t sdim;              // 2 or 3
+  int32_t sg_pow2;           // log2(g) if g is a power of two, else -1
+  int64_t sg;                // grid edge g
+  double scoef[7];           // values by ascending offset
 };
 
 struct SolveConst {

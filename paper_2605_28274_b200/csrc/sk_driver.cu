@@ -132,8 +132,70 @@ bool same_csr(const sk_csr* a, const sk_csr* b) {
          std::memcmp(a->values, b->values, sizeof(double) * a->nnz) == 0;
 }
 
+// Matrix-free stencil detection: the CSR is exactly the Dirichlet-truncated
+// 5-point (2D) or 7-point (3D) grid stencil with one constant value per offset
+// (problems.cpp:10-60 and the 2D sibling). Checked entry by entry, bitwise.
+struct StencilInfo {
+  int dim = 0;
+  int64_t g = 0;
+  double c[7] = {0, 0, 0, 0, 0, 0, 0};
+};
+bool detect_stencil(const int64_t* rp, const int64_t* ci, const double* val, int64_t n, StencilInfo& out) {
+  for (int dim = 2; dim <= 3; ++dim) {
+    int64_t g = dim == 2 ? (int64_t)std::llround(std::sqrt((double)n)) : (int64_t)std::llround(std::cbrt((double)n));
+    if (g < 2 || (dim == 2 ? g * g : g * g * g) != n) continue;
+    const int64_t g2 = g * g;
+    const int nslot = dim == 2 ? 5 : 7;
+    int64_t off[7];
+    if (dim == 2) {
+      const int64_t o[5] = {-g, -1, 0, 1, g};
+      std::memcpy(off, o, sizeof o);
+    } else {
+      const int64_t o[7] = {-g2, -g, -1, 0, 1, g, g2};
+      std::memcpy(off, o, sizeof o);
+    }
+    bool have[7] = {false, false, false, false, false, false, false};
+    double cval[7] = {0, 0, 0, 0, 0, 0, 0};
+    bool ok = true;
+    for (int64_t i = 0; i < n && ok; ++i) {
+      const int64_t ix = i % g, iy = (i / g) % g, iz = i / g2;
+      bool present[7];
+      if (dim == 2) {
+        const bool p[5] = {iy > 0, ix > 0, true, ix < g - 1, iy < g - 1};
+        std::memcpy(present, p, sizeof p);
+      } else {
+        const bool p[7] = {iz > 0, iy > 0, ix > 0, true, ix < g - 1, iy < g - 1, iz < g - 1};
+        std::memcpy(present, p, sizeof p);
+      }
+      int64_t k = rp[i];
+      for (int sl = 0; sl < nslot && ok; ++sl) {
+        if (!present[sl]) continue;
+        if (k >= rp[i + 1] || ci[k] != i + off[sl]) {
+          ok = false;
+          break;
+        }
+        if (!have[sl]) {
+          have[sl] = true;
+          cval[sl] = val[k];
+        } else if (std::memcmp(&cval[sl], &val[k], sizeof(double)) != 0) {
+          ok = false;
+        }
+        ++k;
+      }
+      if (k != rp[i + 1]) ok = false;
+    }
+    if (!ok) continue;
+    out.dim = dim;
+    out.g = g;
+    for (int sl = 0; sl < nslot; ++sl) out.c[sl] = cval[sl];
+    return true;
+  }
+  return false;
+}
+
 struct DevCsr {
   int64_t n = 0, nnz = 0;
+  StencilInfo stencil;
   int32_t* rp = nullptr;
   int32_t* ci = nullptr;
   double* val = nullptr;
@@ -148,6 +210,7 @@ size_t upload_csr(DevCsr& d, int64_t n, int64_t nnz, const int64_t* rp, const in
   for (int64_t k = 0; k < nnz; ++k) ci32[k] = (int32_t)ci[k];
   d.n = n;
   d.nnz = nnz;
+  if (!getenv("SK_NO_STENCIL")) detect_stencil(rp, ci, val, n, d.stencil);
   CK(cudaMalloc(&d.rp, sizeof(int32_t) * (n + 1)));
   CK(cudaMalloc(&d.ci, sizeof(int32_t) * std::max<int64_t>(nnz, 1)));
   CK(cudaMalloc(&d.val, sizeof(double) * std::max<int64_t>(nnz, 1)));
@@ -218,6 +281,7 @@ struct SideBuf {
   int64_t n = 0;
   double *w = nullptr, *wx = nullptr, *qh = nullptr, *hw = nullptr;
   double *hband = nullptr, *coef = nullptr, *coef2 = nullptr, *part = nullptr, *nfac = nullptr;
+  double *mcoef = nullptr, *mcoef2 = nullptr;
   unsigned int* counter = nullptr;
   double** table = nullptr;
   double** table_host = nullptr;  // pinned mirror (async uploads)
@@ -352,7 +416,9 @@ struct Solver {
       b.coef = dalloc<double>(cap_blocks * s * s);
       b.nfac = dalloc<double>(cap_blocks * (s * s + s));
       b.coef2 = dalloc<double>(cap_blocks * s * s);
-      b.part = dalloc<double>(std::max<int64_t>((cap_blocks + 3) * ncta * s * s, nseg + 64));
+      b.mcoef = dalloc<double>(cap_blocks * s * s);
+      b.mcoef2 = dalloc<double>(cap_blocks * s * s);
+      b.part = dalloc<double>(std::max<int64_t>((cap_blocks + 3) * ncta * s * s, 2 * nseg * s * s + 64));
       b.counter = dalloc<unsigned int>(cap_blocks + 8);
       b.table = dalloc<double*>(cap_blocks);
       CK(cudaHostAlloc(&b.table_host, sizeof(double*) * cap_blocks, cudaHostAllocDefault));
@@ -371,10 +437,21 @@ struct Solver {
       sc.coef = b.coef;
       sc.nfac = b.nfac;
       sc.coef2 = b.coef2;
+      sc.mcoef = b.mcoef;
+      sc.mcoef2 = b.mcoef2;
       sc.part = b.part;
       sc.counter = b.counter;
       sc.ncta = ncta;
       sc.nseg = nseg;
+      sc.sdim = op.stencil.dim;
+      sc.sg = op.stencil.g;
+      sc.sg_pow2 = -1;
+      if (op.stencil.g > 0 && (op.stencil.g & (op.stencil.g - 1)) == 0) {
+        int sh = 0;
+        while ((int64_t(1) << sh) < op.stencil.g) ++sh;
+        sc.sg_pow2 = sh;
+      }
+      for (int q = 0; q < 7; ++q) sc.scoef[q] = op.stencil.c[q];
     }
     if (nsides == 1) c.side[1] = c.side[0];
     dstate = dalloc<sk::DevState>(1);
@@ -442,10 +519,26 @@ struct Solver {
                        cudaMemcpyHostToDevice, st));
   }
 
+  double csr_bytes(int sd) const {
+    return P.op[sd].stencil.dim ? 0.0 : 12.0 * P.op[sd].nnz + 4.0 * (P.op[sd].n + 1);
+  }
   double spmm_bytes() const {
     double b = 0;
+    for (int sd = 0; sd < nsides; ++sd) b += csr_bytes(sd) + 16.0 * P.op[sd].n * s;
+    return b;
+  }
+  // algorithmic bytes of the fused Lanczos passes
+  double pass1_bytes(int64_t k) const {
+    const double J = (double)std::min<int64_t>(k + 1, 2);
+    double b = 0;
     for (int sd = 0; sd < nsides; ++sd)
-      b += 12.0 * P.op[sd].nnz + 4.0 * (P.op[sd].n + 1) + 16.0 * P.op[sd].n * s;
+      b += csr_bytes(sd) + 8.0 * P.op[sd].n * s * (J + (P.op[sd].stencil.dim ? 0 : 1));
+    return b;
+  }
+  double pass2_bytes(int64_t k) const {
+    const double J = (double)std::min<int64_t>(k + 1, 2);
+    double b = 0;
+    for (int sd = 0; sd < nsides; ++sd) b += 8.0 * P.op[sd].n * s * (J + 1 + (P.op[sd].stencil.dim ? 0 : 1));
     return b;
   }
   double pass_bytes(int64_t k, int extra) const {
@@ -481,18 +574,26 @@ struct Solver {
     for (auto& e : rev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     int64_t enq = 0, checked = 0;
     bool done = false;
+    const bool fused = sk::lanczos_fused_ok(c) && !getenv("SK_NO_FUSED");
     std::vector<std::vector<double>> caps;
     std::vector<std::pair<int64_t, int64_t>> cap_shape;
     for (int64_t k = 0; k < max_iter && !done; ++k) {
       for (int sd = 0; sd < nsides; ++sd) ensure_blocks(sd, k + 2);
       grow_cores((k + 2) * s);
       const double rp = (double)((k + 1) * s), rq = (double)((k + 2) * s);
-      timed(0, spmm_bytes(), [&] { sk::launch_spmm(c, st); });
-      dbg("spmm", k);
-      timed(1, pass_bytes(k, 1), [&] { sk::launch_lanczos_gram(c, st); });
-      dbg("gram", k);
-      timed(3, pass_bytes(k, 2), [&] { sk::launch_lanczos_update(c, k + 1, st); });
-      dbg("update", k);
+      if (fused) {
+        timed(0, pass1_bytes(k), [&] { sk::launch_lanczos_p1(c, st); });
+        dbg("pass1", k);
+        timed(3, pass2_bytes(k), [&] { sk::launch_lanczos_p2(c, st); });
+        dbg("pass2", k);
+      } else {
+        timed(0, spmm_bytes(), [&] { sk::launch_spmm(c, st); });
+        dbg("spmm", k);
+        timed(1, pass_bytes(k, 1), [&] { sk::launch_lanczos_gram(c, st); });
+        dbg("gram", k);
+        timed(3, pass_bytes(k, 2), [&] { sk::launch_lanczos_update(c, k + 1, st); });
+        dbg("update", k);
+      }
       timed(2, 0.0, [&] { sk::launch_rare(c, k + 1, st); });
       dbg("rare", k);
       timed(4, 8.0 * 3 * rp * rp, [&] { sk::launch_cg_a(c, (k + 1) * s, st); });
@@ -610,6 +711,8 @@ struct Solver {
       dfree(b.hband);
       dfree(b.coef);
       dfree(b.coef2);
+      dfree(b.mcoef);
+      dfree(b.mcoef2);
       dfree(b.part);
       dfree(b.counter);
       dfree(b.table);

@@ -98,6 +98,24 @@ __device__ inline void set_nfac(const SideConst& sc, int64_t b, int s, const dou
   for (int u = 0; u < s; ++u) p[s * s + u] = __ddiv_rn(1.0, p[u * s + u]);
 }
 
+// c = N^{-T} G and M = N^{-1} c (oracle tri_ntinv / tri_ninv), N with 1/diag in nfac
+__device__ inline void block_coefs(const double* nf, const double* G, int s, double* c, double* M) {
+  const double* N = nf;
+  const double* dinv = nf + s * s;
+  for (int u = 0; u < s; ++u)
+    for (int t = 0; t < s; ++t) {
+      double acc = G[u * s + t];
+      for (int r = 0; r < t; ++r) acc = __dsub_rn(acc, __dmul_rn(N[t * s + r], c[u * s + r]));
+      c[u * s + t] = __dmul_rn(acc, dinv[t]);
+    }
+  for (int u = 0; u < s; ++u)
+    for (int t = s - 1; t >= 0; --t) {
+      double acc = c[u * s + t];
+      for (int r = t + 1; r < s; ++r) acc = __dsub_rn(acc, __dmul_rn(N[r * s + t], M[u * s + r]));
+      M[u * s + t] = __dmul_rn(acc, dinv[t]);
+    }
+}
+
 __device__ inline void commit_grow(const SolveConst& c, int side, int grow_stage) {
   const SideConst& sc = c.side[side];
   SideState& st = c.st->side[side];
@@ -270,7 +288,166 @@ __device__ __forceinline__ void unpack_tri(int e, int& t, int& u) {
 }
 
 // =====================================================================
-// K1: SpMM  w = op * V_last   (sparse_matrix.cpp:142-158, order preserved)
+// One row of w = op * V (normalised on the fly): CSR gather or matrix-free
+// stencil. Both accumulate the row's terms in ascending column order with
+// mul+add (sparse_matrix.cpp:151-155), so the stencil form is bitwise the CSR.
+// =====================================================================
+template <int S>
+__device__ __forceinline__ void grid_coords(const SideConst& sc, int64_t i, int64_t& a, int64_t& b,
+                                            int64_t& cz) {
+  // 2D: a = ix, b = iy; 3D: a = ix, b = iy, cz = iz
+  const int64_t g = sc.sg;
+  if (sc.sg_pow2 >= 0) {
+    const int sh = sc.sg_pow2;
+    a = i & (g - 1);
+    const int64_t r = i >> sh;
+    if (sc.sdim == 2) {
+      b = r;
+      cz = 0;
+    } else {
+      b = r & (g - 1);
+      cz = r >> sh;
+    }
+  } else {
+    a = i % g;
+    const int64_t r = i / g;
+    if (sc.sdim == 2) {
+      b = r;
+      cz = 0;
+    } else {
+      b = r % g;
+      cz = r / g;
+    }
+  }
+}
+// raw row of op * U (no normalisation): CSR gather or stencil, ascending columns
+template <int S>
+__device__ __forceinline__ void raw_row_csr(const SideConst& sc, const double* __restrict__ x, int64_t i,
+                                            double* acc, double* own) {
+#pragma unroll
+  for (int u = 0; u < S; ++u) acc[u] = 0.0;
+  const int32_t k0 = __ldg(sc.rp + i), k1 = __ldg(sc.rp + i + 1);
+  for (int32_t kk = k0; kk < k1; ++kk) {
+    const double v = __ldg(sc.val + kk);
+    const int64_t col = __ldg(sc.ci + kk);
+#pragma unroll
+    for (int u = 0; u < S; ++u) acc[u] = __dadd_rn(acc[u], __dmul_rn(v, __ldg(x + col * S + u)));
+  }
+#pragma unroll
+  for (int u = 0; u < S; ++u) own[u] = __ldg(x + i * S + u);
+}
+
+// =====================================================================
+// Raw-block arithmetic contract: the basis is stored as raw
+// blocks U_b with triangular factors N_b (V_b = U_b N_b^{-1}). Per row, only the
+// operator output is normalised: w = (op U_{k-1}) N_{k-1}^{-1}. Gram sums run on
+// raw blocks, G_b = U_b^T x (R1), then c_b = N_b^{-T} G_b and M_b = N_b^{-1} c_b
+// are formed once per block; updates are x - sum_b U_b M_b.
+// =====================================================================
+constexpr int kFusedSegsPerCta = 8;
+
+template <int S>
+__device__ __forceinline__ void ld_raw(const double* __restrict__ x, int64_t i, double* u) {
+  if constexpr (S % 2 == 0) {
+    const double2* p = reinterpret_cast<const double2*>(x + i * S);
+#pragma unroll
+    for (int h = 0; h < S / 2; ++h) {
+      const double2 v = __ldg(p + h);
+      u[2 * h] = v.x;
+      u[2 * h + 1] = v.y;
+    }
+  } else {
+#pragma unroll
+    for (int t = 0; t < S; ++t) u[t] = __ldg(x + i * S + t);
+  }
+}
+template <int S>
+__device__ __forceinline__ void ld_raw_cg(const double* __restrict__ x, int64_t i, double* u) {
+  if constexpr (S % 2 == 0) {
+    const double2* p = reinterpret_cast<const double2*>(x + i * S);
+#pragma unroll
+    for (int h = 0; h < S / 2; ++h) {
+      const double2 v = __ldcg(p + h);
+      u[2 * h] = v.x;
+      u[2 * h + 1] = v.y;
+    }
+  } else {
+#pragma unroll
+    for (int t = 0; t < S; ++t) u[t] = __ldcg(x + i * S + t);
+  }
+}
+template <int S>
+__device__ __forceinline__ void st_row(double* __restrict__ x, int64_t i, const double* y) {
+  if constexpr (S % 2 == 0) {
+    double2* p = reinterpret_cast<double2*>(x + i * S);
+#pragma unroll
+    for (int h = 0; h < S / 2; ++h) p[h] = make_double2(y[2 * h], y[2 * h + 1]);
+  } else {
+#pragma unroll
+    for (int t = 0; t < S; ++t) x[i * S + t] = y[t];
+  }
+}
+
+// Matrix-free stencil row of op * U (raw): all neighbours loaded unconditionally
+// (clamped addresses), absent ones skipped by selects -- exactly the CSR order.
+template <int S, int DIM>
+__device__ __forceinline__ void stencil_row(const SideConst& sc, const double* __restrict__ x, int64_t i,
+                                            double* acc, double* own) {
+  constexpr int K = DIM == 2 ? 5 : 7;
+  constexpr int C = DIM == 2 ? 2 : 3;
+  int64_t ix, iy, iz;
+  grid_coords<S>(sc, i, ix, iy, iz);
+  const int64_t g = sc.sg, g2 = g * g;
+  bool pr[K];
+  int64_t col[K];
+  if (DIM == 2) {
+    pr[0] = iy > 0; col[0] = i - g;
+    pr[1] = ix > 0; col[1] = i - 1;
+    pr[2] = true;   col[2] = i;
+    pr[3] = ix < g - 1; col[3] = i + 1;
+    pr[4] = iy < g - 1; col[4] = i + g;
+  } else {
+    pr[0] = iz > 0; col[0] = i - g2;
+    pr[1] = iy > 0; col[1] = i - g;
+    pr[2] = ix > 0; col[2] = i - 1;
+    pr[3] = true;   col[3] = i;
+    pr[4] = ix < g - 1; col[4] = i + 1;
+    pr[5] = iy < g - 1; col[5] = i + g;
+    pr[6] = iz < g - 1; col[6] = i + g2;
+  }
+  double u[K][S];
+#pragma unroll
+  for (int k = 0; k < K; ++k) ld_raw<S>(x, pr[k] ? col[k] : i, u[k]);
+#pragma unroll
+  for (int t = 0; t < S; ++t) {
+    acc[t] = 0.0;
+    own[t] = u[C][t];
+  }
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    const double v = sc.scoef[k];
+#pragma unroll
+    for (int t = 0; t < S; ++t) {
+      const double nv = __dadd_rn(acc[t], __dmul_rn(v, u[k][t]));
+      acc[t] = pr[k] ? nv : acc[t];
+    }
+  }
+}
+
+// w row (normalised) and the raw own row of U_{k-1}
+template <int S, int MODE>
+__device__ __forceinline__ void w_row(const SideConst& sc, const double* __restrict__ x, const NF<S>& f,
+                                      int64_t i, double* w, double* own) {
+  double acc[S];
+  if constexpr (MODE == 2 || MODE == 3)
+    stencil_row<S, MODE>(sc, x, i, acc, own);
+  else
+    raw_row_csr<S>(sc, x, i, acc, own);
+  norm_row<S>(acc, f, w);
+}
+
+// =====================================================================
+// K1: SpMM  w = (op U_{k-1}) N^{-1}   (sparse_matrix.cpp:142-158, order kept)
 // =====================================================================
 template <int S>
 __global__ void __launch_bounds__(256) k_spmm(SolveConst c) {
@@ -285,35 +462,92 @@ __global__ void __launch_bounds__(256) k_spmm(SolveConst c) {
   const double* __restrict__ x = sc.blocks[kl];
   NF<S> f;
   load_nf<S>(sc.nfac, kl, f);
-  double* __restrict__ w = sc.w;
   const int64_t n = sc.n;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
-    double acc[S];
-#pragma unroll
-    for (int u = 0; u < S; ++u) acc[u] = 0.0;
-    const int32_t k0 = __ldg(sc.rp + i), k1 = __ldg(sc.rp + i + 1);
-    for (int32_t kk = k0; kk < k1; ++kk) {
-      const int64_t col = __ldg(sc.ci + kk);
-      const double v = __ldg(sc.val + kk);
-      double q[S];
-      load_vrow<S>(x, f, col, q);
-#pragma unroll
-      for (int u = 0; u < S; ++u) acc[u] = __dadd_rn(acc[u], __dmul_rn(v, q[u]));
-    }
-#pragma unroll
-    for (int u = 0; u < S; ++u) w[i * S + u] = acc[u];
+    double y[S], own[S];
+    if (sc.sdim == 2)
+      w_row<S, 2>(sc, x, f, i, y, own);
+    else if (sc.sdim == 3)
+      w_row<S, 3>(sc, x, f, i, y, own);
+    else
+      w_row<S, 0>(sc, x, f, i, y, own);
+    st_row<S>(sc.w, i, y);
   }
 }
 
 // =====================================================================
-// K2: R1 Gram of x against blocks [b0, b1). One CTA per (row group, block).
+// Canonical-tree helpers for one-warp-per-segment kernels
+// =====================================================================
+__device__ __forceinline__ double tree32(double* a) {
+#pragma unroll
+  for (int w = 16; w >= 1; w >>= 1)
+#pragma unroll
+    for (int i = 0; i < w; ++i) a[i] = __dadd_rn(a[2 * i], a[2 * i + 1]);
+  return a[0];
+}
+// Canonical tree over P CTA partials part[p*NE + e] for every e (last CTA):
+// aligned groups of 32 in registers, then the group nodes in smem.
+template <int NE>
+__device__ void final_tree(const double* part, int64_t P, double* out) {
+  constexpr int MAXG = 128;
+  __shared__ double gnode[NE][MAXG];
+  const int64_t ngroups = (P + 31) / 32;
+  if (ngroups > MAXG) {
+    for (int e = threadIdx.x; e < NE; e += blockDim.x) out[e] = tree_stream(part + e, P, NE);
+    __syncthreads();
+    return;
+  }
+  for (int64_t idx = threadIdx.x; idx < NE * ngroups; idx += blockDim.x) {
+    const int e = (int)(idx % NE);
+    const int64_t grp = idx / NE;
+    const int64_t p0 = grp * 32;
+    const int cnt = (int)mn64(32, P - p0);
+    double a[32];
+    if (cnt == 32) {
+#pragma unroll
+      for (int j = 0; j < 32; ++j) a[j] = __ldcg(part + (p0 + j) * NE + e);
+      gnode[e][grp] = tree32(a);
+    } else {
+      gnode[e][grp] = tree_stream(part + p0 * NE + e, cnt, NE);
+    }
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < NE; e += blockDim.x) {
+    TreeStream ts;
+    ts.init();
+    for (int64_t grp = 0; grp < ngroups; ++grp) ts.push(gnode[e][grp]);
+    out[e] = ts.finish();
+  }
+  __syncthreads();
+}
+template <int NE>
+__device__ __forceinline__ void warp_seg_to_cta(const double* acc, int nvalid_cta, double* part_out) {
+  __shared__ double snode[kFusedSegsPerCta][NE];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int e = 0; e < NE; ++e) {
+    const double v = butterfly(acc[e]);
+    if (lane == (e & 31)) snode[warp][e] = v;
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < NE; e += blockDim.x) {
+    double a[kFusedSegsPerCta];
+#pragma unroll
+    for (int w = 0; w < kFusedSegsPerCta; ++w) a[w] = snode[w][e];
+    part_out[e] = tree_reduce_local(a, nvalid_cta);
+  }
+}
+
+// =====================================================================
+// K2: R1 Gram G_b = U_b^T x against blocks [b0, b1); one CTA per (row group,
+// block); the last CTA of each block forms c_b = N_b^{-T} G_b and M_b.
 // =====================================================================
 enum GramMode : int { GM_J = 0, GM_ALL_W = 1, GM_ALL_X = 2, GM_CLEAN = 3 };
 
 template <int S>
 __device__ inline bool gram_setup(const SolveConst& c, int side, int mode, const double*& x,
-                                  double*& out, int64_t& b0, int64_t& b1) {
+                                  double*& out, double*& mout, int64_t& b0, int64_t& b1) {
   const DevState* st = c.st;
   if (st->status != RUNNING) return false;
   const SideState& ss = st->side[side];
@@ -323,6 +557,7 @@ __device__ inline bool gram_setup(const SolveConst& c, int side, int mode, const
     if (ss.stage != ST_NEED_CLEANUP) return false;
     x = sc.blocks[k];
     out = sc.coef2;
+    mout = sc.mcoef2;
     b0 = 0;
     b1 = k;
     return true;
@@ -332,18 +567,21 @@ __device__ inline bool gram_setup(const SolveConst& c, int side, int mode, const
     case GM_J:
       x = sc.w;
       out = sc.coef;
+      mout = sc.mcoef;
       b0 = first_block(c, k);
       b1 = k;
       return true;
     case GM_ALL_W:
       x = sc.w;
       out = sc.coef;
+      mout = sc.mcoef;
       b0 = 0;
       b1 = k;
       return true;
     case GM_ALL_X:
       x = sc.wx;
       out = sc.coef2;
+      mout = sc.mcoef2;
       b0 = 0;
       b1 = k;
       return true;
@@ -357,9 +595,9 @@ __global__ void __launch_bounds__(256) k_gram(SolveConst c, int mode) {
   const int side = blockIdx.z;
   if (side >= c.nsides) return;
   const double* x;
-  double* out;
+  double *out, *mout;
   int64_t b0, b1;
-  if (!gram_setup<S>(c, side, mode, x, out, b0, b1)) return;
+  if (!gram_setup<S>(c, side, mode, x, out, mout, b0, b1)) return;
   const SideConst& sc = c.side[side];
   const int64_t nblk = b1 - b0;
   const int64_t by = blockIdx.y;
@@ -367,9 +605,7 @@ __global__ void __launch_bounds__(256) k_gram(SolveConst c, int mode) {
   const int64_t cta = blockIdx.x;
   if (cta >= sc.ncta) return;
   const int64_t b = b0 + by;
-  const double* __restrict__ vb = sc.blocks[b];
-  NF<S> f;
-  load_nf<S>(sc.nfac, b, f);
+  const double* __restrict__ ub = sc.blocks[b];
   const int lane = threadIdx.x & 31;
   const int64_t n = sc.n;
   const SegGeom g = seg_geom(cta, sc.nseg);
@@ -387,9 +623,8 @@ __global__ void __launch_bounds__(256) k_gram(SolveConst c, int mode) {
         const int64_t i = base + lane + 32 * m;
         if (i < n) {
           double a[S], y[S];
-          load_vrow<S>(vb, f, i, a);
-#pragma unroll
-          for (int t = 0; t < S; ++t) y[t] = __ldg(x + i * S + t);
+          ld_raw<S>(ub, i, a);
+          ld_raw<S>(x, i, y);
 #pragma unroll
           for (int u = 0; u < S; ++u)
 #pragma unroll
@@ -402,23 +637,281 @@ __global__ void __launch_bounds__(256) k_gram(SolveConst c, int mode) {
   }
   cta_combine<NB>(segv, g.nvalid_warp, g.nvalid_cta, part);
 
-  // level 1: the last CTA of this (side, block) reduces over row groups
-  unsigned int* ctr = sc.counter;  // slots: 0 side-level, 1 update, 2.. per block
-  if (!last_cta_arrive(ctr + 2 + by, (unsigned)sc.ncta)) return;
-  for (int e = threadIdx.x; e < NB; e += blockDim.x) {
-    const double v = tree_stream(sc.part + by * sc.ncta * NB + e, sc.ncta, NB);
-    out[b * NB + e] = v;
+  unsigned int* ctr = sc.counter;  // slots: 0 pass 1, 1 update, 2 clean-up, 4.. per block
+  if (!last_cta_arrive(ctr + 4 + by, (unsigned)sc.ncta)) return;
+  __shared__ double G[NB];
+  for (int e = threadIdx.x; e < NB; e += blockDim.x)
+    G[e] = tree_stream(sc.part + by * sc.ncta * NB + e, sc.ncta, NB);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double cb[NB], mb[NB];
+    block_coefs(sc.nfac + b * (NB + S), G, S, cb, mb);
+    for (int e = 0; e < NB; ++e) {
+      out[b * NB + e] = cb[e];
+      mout[b * NB + e] = mb[e];
+    }
     if (mode == GM_ALL_X && c.arnoldi) {
       // H column = first + second CGS pass (block_krylov.cpp:87-93)
-      const int t = e % S, u = e / S;
-      const double h = __dadd_rn(__ldcg(sc.coef + b * NB + e), v);
-      hcol_ptr(sc, c.st->side[side].steps, u, S)[b * S + t] = h;
+      for (int e = 0; e < NB; ++e) {
+        const int t = e % S, u = e / S;
+        hcol_ptr(sc, c.st->side[side].steps, u, S)[b * S + t] = __dadd_rn(__ldcg(sc.coef + b * NB + e), cb[e]);
+      }
     }
   }
 }
 
 // =====================================================================
-// x_out = x_in - sum_{b in [b0,b1)} V_b c_b (+ R1 Gram of x_out, finalise)
+// Fused Lanczos passes (S <= 4). One warp per R1 segment, 8 warps per CTA
+// (the CTA node is the canonical tree's level-3 node).
+// =====================================================================
+template <int S, int MODE>
+__device__ __forceinline__ void p1_body(const SideConst& sc, const double* __restrict__ u1, const NF<S>& f1,
+                                        const double* __restrict__ u0, bool two, int64_t base, int64_t n,
+                                        double* acc) {
+  constexpr int NB = S * S;
+  const int lane = threadIdx.x & 31;
+#pragma unroll 4
+  for (int m = 0; m < kLRows; ++m) {
+    const int64_t i = base + lane + 32 * m;
+    if (i < n) {
+      double y[S], a1[S], a0[S];
+      w_row<S, MODE>(sc, u1, f1, i, y, a1);
+      if (MODE == 0) st_row<S>(sc.w, i, y);
+      if (two) ld_raw<S>(u0, i, a0);
+#pragma unroll
+      for (int u = 0; u < S; ++u)
+#pragma unroll
+        for (int t = 0; t < S; ++t) {
+          if (two) acc[u * S + t] = __dadd_rn(acc[u * S + t], __dmul_rn(a0[t], y[u]));
+          acc[NB + u * S + t] = __dadd_rn(acc[NB + u * S + t], __dmul_rn(a1[t], y[u]));
+        }
+    }
+  }
+}
+
+// Lanczos pass 1: w = (op U_{k-1}) N_{k-1}^{-1}; G = U_{k-2}^T w, U_{k-1}^T w
+// (block_krylov.cpp:71-84, CGS form). w is stored only for CSR operators.
+template <int S>
+__global__ void __launch_bounds__(256, 4) k_lanczos_p1(SolveConst c) {
+  constexpr int NB = S * S;
+  constexpr int NE = 2 * NB;
+  const int side = blockIdx.z;
+  if (side >= c.nsides) return;
+  const DevState* st = c.st;
+  if (st->status != RUNNING) return;
+  const SideState& ss = st->side[side];
+  if (ss.exhausted || ss.broken) return;
+  const SideConst& sc = c.side[side];
+  const int64_t nseg = sc.nseg;
+  const int64_t ncta = (nseg + kFusedSegsPerCta - 1) / kFusedSegsPerCta;
+  const int64_t cta = blockIdx.x;
+  if (cta >= ncta) return;
+  const int64_t k = ss.blocks;
+  const bool two = k >= 2;
+  const double* __restrict__ u1 = sc.blocks[k - 1];
+  const double* __restrict__ u0 = two ? sc.blocks[k - 2] : u1;
+  NF<S> f1;
+  load_nf<S>(sc.nfac, k - 1, f1);
+  const int warp = threadIdx.x >> 5;
+  const int64_t seg = cta * kFusedSegsPerCta + warp;
+  const int nvalid_cta = (int)mn64(kFusedSegsPerCta, nseg - cta * kFusedSegsPerCta);
+  double acc[NE];
+#pragma unroll
+  for (int e = 0; e < NE; ++e) acc[e] = 0.0;
+  if (seg < nseg) {
+    const int64_t base = seg * kSeg;
+    if (sc.sdim == 2)
+      p1_body<S, 2>(sc, u1, f1, u0, two, base, sc.n, acc);
+    else if (sc.sdim == 3)
+      p1_body<S, 3>(sc, u1, f1, u0, two, base, sc.n, acc);
+    else
+      p1_body<S, 0>(sc, u1, f1, u0, two, base, sc.n, acc);
+  }
+  warp_seg_to_cta<NE>(acc, nvalid_cta, sc.part + cta * NE);
+  if (!last_cta_arrive(sc.counter + 0, (unsigned)ncta)) return;
+  __shared__ double res[NE];
+  final_tree<NE>(sc.part, ncta, res);
+  if (threadIdx.x < 2) {
+    const int slot = threadIdx.x;  // 0: block k-2, 1: block k-1
+    if (slot == 1 || two) {
+      const int64_t b = slot == 0 ? k - 2 : k - 1;
+      double cb[NB], mb[NB];
+      block_coefs(sc.nfac + b * (NB + S), res + slot * NB, S, cb, mb);
+      for (int e = 0; e < NB; ++e) {
+        sc.coef[b * NB + e] = cb[e];
+        sc.mcoef[b * NB + e] = mb[e];
+      }
+    }
+  }
+}
+
+template <int S, int MODE>
+__device__ __forceinline__ void p2_body(const SideConst& sc, const double* __restrict__ u1, const NF<S>& f1,
+                                        const double* __restrict__ u0, bool two, const double* m1,
+                                        const double* m0, double* __restrict__ out, int64_t base, int64_t n,
+                                        double* acc) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll 4
+  for (int m = 0; m < kLRows; ++m) {
+    const int64_t i = base + lane + 32 * m;
+    if (i < n) {
+      double y[S], a1[S], a0[S];
+      if (MODE == 0) {
+        ld_raw_cg<S>(sc.w, i, y);
+        ld_raw<S>(u1, i, a1);
+      } else {
+        w_row<S, MODE>(sc, u1, f1, i, y, a1);
+      }
+      if (two) {
+        ld_raw<S>(u0, i, a0);
+#pragma unroll
+        for (int u = 0; u < S; ++u) {
+          double tmp = 0.0;
+#pragma unroll
+          for (int t = 0; t < S; ++t) tmp = __dadd_rn(tmp, __dmul_rn(a0[t], m0[u * S + t]));
+          y[u] = __dsub_rn(y[u], tmp);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < S; ++u) {
+        double tmp = 0.0;
+#pragma unroll
+        for (int t = 0; t < S; ++t) tmp = __dadd_rn(tmp, __dmul_rn(a1[t], m1[u * S + t]));
+        y[u] = __dsub_rn(y[u], tmp);
+      }
+      st_row<S>(out, i, y);
+      int e = 0;
+#pragma unroll
+      for (int u = 0; u < S; ++u)
+#pragma unroll
+        for (int t = 0; t <= u; ++t) {
+          acc[e] = __dadd_rn(acc[e], __dmul_rn(y[t], y[u]));
+          ++e;
+        }
+    }
+  }
+}
+
+// Lanczos pass 2: U_k = w - U_{k-2} M_{k-2} - U_{k-1} M_{k-1} (+ R1 self Gram,
+// finalise). Matrix-free operators recompute w from U_{k-1} instead of reading it.
+template <int S>
+__global__ void __launch_bounds__(256, 4) k_lanczos_p2(SolveConst c) {
+  constexpr int NS = S * (S + 1) / 2;
+  const int side = blockIdx.z;
+  if (side >= c.nsides) return;
+  const DevState* st = c.st;
+  if (st->status != RUNNING) return;
+  const SideState& ss = st->side[side];
+  if (ss.exhausted || ss.broken) return;
+  const SideConst& sc = c.side[side];
+  const int64_t nseg = sc.nseg;
+  const int64_t ncta = (nseg + kFusedSegsPerCta - 1) / kFusedSegsPerCta;
+  const int64_t cta = blockIdx.x;
+  if (cta >= ncta) return;
+  const int64_t k = ss.blocks;
+  const bool two = k >= 2;
+  const double* __restrict__ u1 = sc.blocks[k - 1];
+  const double* __restrict__ u0 = two ? sc.blocks[k - 2] : u1;
+  NF<S> f1;
+  load_nf<S>(sc.nfac, k - 1, f1);
+  double m1[S * S], m0[S * S];
+#pragma unroll
+  for (int e = 0; e < S * S; ++e) {
+    m1[e] = __ldcg(sc.mcoef + (k - 1) * S * S + e);
+    m0[e] = two ? __ldcg(sc.mcoef + (k - 2) * S * S + e) : 0.0;
+  }
+  double* __restrict__ out = sc.blocks[k];
+  const int warp = threadIdx.x >> 5;
+  const int64_t seg = cta * kFusedSegsPerCta + warp;
+  const int nvalid_cta = (int)mn64(kFusedSegsPerCta, nseg - cta * kFusedSegsPerCta);
+  double acc[NS];
+#pragma unroll
+  for (int e = 0; e < NS; ++e) acc[e] = 0.0;
+  if (seg < nseg) {
+    const int64_t base = seg * kSeg;
+    if (sc.sdim == 2)
+      p2_body<S, 2>(sc, u1, f1, u0, two, m1, m0, out, base, sc.n, acc);
+    else if (sc.sdim == 3)
+      p2_body<S, 3>(sc, u1, f1, u0, two, m1, m0, out, base, sc.n, acc);
+    else
+      p2_body<S, 0>(sc, u1, f1, u0, two, m1, m0, out, base, sc.n, acc);
+  }
+  warp_seg_to_cta<NS>(acc, nvalid_cta, sc.part + cta * NS);
+  if (!last_cta_arrive(sc.counter + 1, (unsigned)ncta)) return;
+  __shared__ double res[NS];
+  final_tree<NS>(sc.part, ncta, res);
+  SideState& sst = c.st->side[side];
+  for (int e = threadIdx.x; e < NS; e += blockDim.x) {
+    int t, u;
+    unpack_tri(e, t, u);
+    sst.gbase[u * S + t] = res[e];
+    sst.gbase[t * S + u] = res[e];
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) finalize_direct(c, side, true);
+}
+
+// Clean-up Gram (rare path): each CTA sweeps all blocks for its row group, so
+// the no-op launch stays one CTA per row group.
+template <int S>
+__global__ void __launch_bounds__(256) k_gram_loop(SolveConst c) {
+  constexpr int NB = S * S;
+  const int side = blockIdx.z;
+  if (side >= c.nsides) return;
+  const DevState* st = c.st;
+  if (st->status != RUNNING) return;
+  const SideState& ss = st->side[side];
+  if (ss.stage != ST_NEED_CLEANUP) return;
+  const SideConst& sc = c.side[side];
+  const int64_t cta = blockIdx.x;
+  if (cta >= sc.ncta) return;
+  const int64_t k = ss.blocks;
+  const double* __restrict__ x = sc.blocks[k];
+  const int lane = threadIdx.x & 31;
+  const int64_t n = sc.n;
+  const SegGeom g = seg_geom(cta, sc.nseg);
+  for (int64_t b = 0; b < k; ++b) {
+    const double* __restrict__ ub = sc.blocks[b];
+    OwnerVals<NB> segv[kSegsPerWarp];
+    for (int q = 0; q < kSegsPerWarp; ++q) {
+      double acc[NB];
+#pragma unroll
+      for (int e = 0; e < NB; ++e) acc[e] = 0.0;
+      if (q < g.nvalid_warp) {
+        const int64_t base = (g.seg_w0 + q) * kSeg;
+        for (int m = 0; m < kLRows; ++m) {
+          const int64_t i = base + lane + 32 * m;
+          if (i < n) {
+            double a[S], y[S];
+            ld_raw<S>(ub, i, a);
+#pragma unroll
+            for (int t = 0; t < S; ++t) y[t] = x[i * S + t];
+#pragma unroll
+            for (int u = 0; u < S; ++u)
+#pragma unroll
+              for (int t = 0; t < S; ++t) acc[u * S + t] = __dadd_rn(acc[u * S + t], __dmul_rn(a[t], y[u]));
+          }
+        }
+      }
+      seg_butterfly<NB>(acc, segv[q], lane);
+    }
+    cta_combine<NB>(segv, g.nvalid_warp, g.nvalid_cta, sc.part + (b * sc.ncta + cta) * NB);
+    __syncthreads();
+  }
+  if (!last_cta_arrive(sc.counter + 2, (unsigned)sc.ncta)) return;
+  for (int64_t b = threadIdx.x; b < k; b += blockDim.x) {
+    double G[NB], cb[NB], mb[NB];
+    for (int e = 0; e < NB; ++e) G[e] = tree_stream(sc.part + b * sc.ncta * NB + e, sc.ncta, NB);
+    block_coefs(sc.nfac + b * (NB + S), G, S, cb, mb);
+    for (int e = 0; e < NB; ++e) {
+      sc.coef2[b * NB + e] = cb[e];
+      sc.mcoef2[b * NB + e] = mb[e];
+    }
+  }
+}
+
+// =====================================================================
+// x_out = x_in - sum_{b in [b0,b1)} U_b M_b (+ R1 Gram of x_out, finalise)
 // =====================================================================
 enum UpdMode : int { UM_LANCZOS = 0, UM_FIRST = 1, UM_SECOND = 2, UM_CLEAN = 3, UM_INIT = 4 };
 
@@ -433,7 +926,7 @@ __global__ void __launch_bounds__(256) k_update(SolveConst c, int mode) {
   const SideConst& sc = c.side[side];
   const int64_t k = ss.blocks;
   const double* xin;
-  const double* coef = sc.coef;
+  const double* mc = sc.mcoef;
   double* xout;
   int64_t b0 = 0, b1 = 0;
   bool gram = true;
@@ -457,7 +950,7 @@ __global__ void __launch_bounds__(256) k_update(SolveConst c, int mode) {
       if (ss.exhausted || ss.broken) return;
       xin = sc.wx;
       xout = sc.blocks[k];
-      coef = sc.coef2;
+      mc = sc.mcoef2;
       b0 = 0;
       b1 = k;
       break;
@@ -465,7 +958,7 @@ __global__ void __launch_bounds__(256) k_update(SolveConst c, int mode) {
       if (ss.stage != ST_NEED_CLEANUP) return;
       xin = sc.blocks[k];
       xout = sc.blocks[k];
-      coef = sc.coef2;
+      mc = sc.mcoef2;
       b0 = 0;
       b1 = k;
       break;
@@ -493,24 +986,20 @@ __global__ void __launch_bounds__(256) k_update(SolveConst c, int mode) {
         const int64_t i = base + lane + 32 * m;
         if (i < n) {
           double y[S];
-#pragma unroll
-          for (int u = 0; u < S; ++u) y[u] = __ldcg(xin + i * S + u);
+          ld_raw_cg<S>(xin, i, y);
           for (int64_t b = b0; b < b1; ++b) {
-            NF<S> f;
-            load_nf<S>(sc.nfac, b, f);
             double a[S];
-            load_vrow<S>(sc.blocks[b], f, i, a);
-            const double* cb = coef + b * (S * S);
+            ld_raw<S>(sc.blocks[b], i, a);
+            const double* mb = mc + b * (S * S);
 #pragma unroll
             for (int u = 0; u < S; ++u) {
               double tmp = 0.0;
 #pragma unroll
-              for (int t = 0; t < S; ++t) tmp = __dadd_rn(tmp, __dmul_rn(a[t], __ldg(cb + u * S + t)));
+              for (int t = 0; t < S; ++t) tmp = __dadd_rn(tmp, __dmul_rn(a[t], __ldg(mb + u * S + t)));
               y[u] = __dsub_rn(y[u], tmp);
             }
           }
-#pragma unroll
-          for (int u = 0; u < S; ++u) xout[i * S + u] = y[u];
+          st_row<S>(xout, i, y);
           int e = 0;
 #pragma unroll
           for (int u = 0; u < S; ++u)
@@ -1070,6 +1559,9 @@ struct Launch {
   static void gram(const SolveConst& c, int mode, int64_t nblk, cudaStream_t st);
   static void update(const SolveConst& c, int mode, cudaStream_t st);
   static void householder(const SolveConst& c, int which, cudaStream_t st);
+  static void lanczos_p1(const SolveConst& c, cudaStream_t st);
+  static void lanczos_p2(const SolveConst& c, cudaStream_t st);
+  static void gram_loop(const SolveConst& c, cudaStream_t st);
   static void cg_a(const SolveConst& c, int64_t rmax, cudaStream_t st);
   static void cg_b(const SolveConst& c, int64_t rmax, cudaStream_t st);
   static void spmm_plain(const int32_t* rp, const int32_t* ci, const double* val, const double* x,
@@ -1104,6 +1596,22 @@ struct Launch {
   }
   static void householder(const SolveConst& c, int which, cudaStream_t st) {
     k_householder<S><<<c.nsides, 1024, 0, st>>>(c, which);
+  }
+  static unsigned fused_grid(const SolveConst& c) {
+    int64_t m = 0;
+    for (int s = 0; s < c.nsides; ++s) m = mx64(m, (c.side[s].nseg + kFusedSegsPerCta - 1) / kFusedSegsPerCta);
+    return (unsigned)m;
+  }
+  static void lanczos_p1(const SolveConst& c, cudaStream_t st) {
+    if constexpr (S <= 4) k_lanczos_p1<S><<<dim3(fused_grid(c), 1, c.nsides), 256, 0, st>>>(c);
+  }
+  static void lanczos_p2(const SolveConst& c, cudaStream_t st) {
+    if constexpr (S <= 4) k_lanczos_p2<S><<<dim3(fused_grid(c), 1, c.nsides), 256, 0, st>>>(c);
+  }
+  static void gram_loop(const SolveConst& c, cudaStream_t st) {
+    int64_t nmax, cmax;
+    dims(c, nmax, cmax);
+    k_gram_loop<S><<<dim3((unsigned)cmax, 1, c.nsides), 256, 0, st>>>(c);
   }
   static void cg_a(const SolveConst& c, int64_t rmax, cudaStream_t st) {
     const unsigned nt = (unsigned)((rmax + kTile - 1) / kTile);
@@ -1159,6 +1667,15 @@ void launch_lanczos_gram(const SolveConst& c, cudaStream_t st) {
   SK_DISPATCH_S(c.s, gram(c, (int)GM_J, 2, st));
   g_launches += 1;
 }
+bool lanczos_fused_ok(const SolveConst& c) { return c.s <= 4 && !c.full_reorth; }
+void launch_lanczos_p1(const SolveConst& c, cudaStream_t st) {
+  SK_DISPATCH_S(c.s, lanczos_p1(c, st));
+  g_launches += 1;
+}
+void launch_lanczos_p2(const SolveConst& c, cudaStream_t st) {
+  SK_DISPATCH_S(c.s, lanczos_p2(c, st));
+  g_launches += 1;
+}
 void launch_lanczos_update(const SolveConst& c, int64_t kmax_blocks, cudaStream_t st) {
   if (c.full_reorth) {
     SK_DISPATCH_S(c.s, update(c, (int)UM_FIRST, st));
@@ -1172,7 +1689,8 @@ void launch_lanczos_update(const SolveConst& c, int64_t kmax_blocks, cudaStream_
 }
 void launch_rare(const SolveConst& c, int64_t kmax_blocks, cudaStream_t st) {
   SK_DISPATCH_S(c.s, householder(c, 0, st));
-  SK_DISPATCH_S(c.s, gram(c, (int)GM_CLEAN, kmax_blocks, st));
+  (void)kmax_blocks;
+  SK_DISPATCH_S(c.s, gram_loop(c, st));
   SK_DISPATCH_S(c.s, update(c, (int)UM_CLEAN, st));
   SK_DISPATCH_S(c.s, householder(c, 1, st));
   g_launches += 4;

@@ -10,6 +10,9 @@ void launch_count_reset();
 void launch_init(const SolveConst& c, const double* dc1, const double* dc2, cudaStream_t st);
 void launch_spmm(const SolveConst& c, cudaStream_t st);
 void launch_lanczos_gram(const SolveConst& c, cudaStream_t st);
+bool lanczos_fused_ok(const SolveConst& c);
+void launch_lanczos_p1(const SolveConst& c, cudaStream_t st);
+void launch_lanczos_p2(const SolveConst& c, cudaStream_t st);
 void launch_lanczos_update(const SolveConst& c, int64_t kmax_blocks, cudaStream_t st);
 void launch_rare(const SolveConst& c, int64_t kmax_blocks, cudaStream_t st);
 void launch_arnoldi_ext(const SolveConst& c, int64_t kmax_blocks, cudaStream_t st);

@@ -114,3 +114,41 @@ def test_history_within_reference_order_tolerance(sk, po):
     h = sol.history.rel_residuals()
     assert h.size == ref.rel_residual.size
     assert max_rel(h[:21], ref.rel_residual[:21]) <= 1e-10
+
+
+@pytest.mark.parametrize("env", ["SK_NO_STENCIL", "SK_NO_FUSED"])
+def test_kernel_variants_bitwise(sk, po, env, monkeypatch):
+    """Matrix-free stencil vs CSR gather, fused vs generic Lanczos passes: identical bits."""
+    a = po.laplacian_2d(40)
+    c1, c2 = po.random_rhs(1600, 2, 5), po.random_rhs(1600, 2, 6)
+    A = to_sk(sk, a)
+    base = sk.factorized_cg(A, A, c1, c2, sk.SolverConfig(eps_tol=1e-9))
+    monkeypatch.setenv(env, "1")
+    alt = sk.factorized_cg(A, A, c1, c2, sk.SolverConfig(eps_tol=1e-9))
+    assert bits_equal(base.history.rel_residuals(), alt.history.rel_residuals())
+    assert bits_equal(base.core, alt.core) and bits_equal(base.V, alt.V)
+    ref = po.factorized_cg(a, a, c1, c2, po.Config(eps_tol=1e-9), po.REPRODUCIBLE)
+    assert bits_equal(base.history.rel_residuals(), ref.rel_residual)
+
+
+def test_convection_diffusion_3d_stencil_cg_lyapunov_s4(sk, po):
+    """3D stencil path (7-point, nonsymmetric values rejected for CG) and s=4."""
+    a = po.convection_diffusion_3d(6, (0.0, 0.0, 0.0))
+    c1 = po.random_rhs(216, 4, 9)
+    ref = po.factorized_cg_lyapunov(a, c1, po.Config(eps_tol=1e-9), po.REPRODUCIBLE)
+    sol = sk.factorized_cg_lyapunov(to_sk(sk, a), c1, sk.SolverConfig(eps_tol=1e-9))
+    _compare(sol, ref)
+
+
+def test_golden_history_fixture(sk, po):
+    """Config 1 against the committed golden fixture (no oracle run needed on the box)."""
+    import json, os
+    g = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "histories.json")))
+    from paper_2605_28274_b200.problems import baseline_config
+    cfg = baseline_config(1)
+    sol = sk.factorized_cg(cfg.a, cfg.b, cfg.c1, cfg.c2, sk.SolverConfig(eps_tol=1e-8, max_iter=500))
+    h = sol.history.rel_residuals()
+    assert h.tolist() == g["config1_cg_reproducible"]["rel_residual"]
+    f = np.array(g["config1_cg_reference_order"]["rel_residual"])
+    assert h.size == f.size
+    assert max_rel(h, f) <= 1e-10
