@@ -47,7 +47,7 @@ def _compile(unit, verbose):
                "-c", os.path.join(CSRC, src), "-o", os.path.join(CSRC, obj)]
     else:
         cmd = [NVCC, *FLAGS, *defs, "-c", os.path.join(CSRC, src), "-o", os.path.join(CSRC, obj)]
-    if verbose:
+    if verbose and not src.endswith(".cpp"):
         cmd.insert(1, "-Xptxas=-v")
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:

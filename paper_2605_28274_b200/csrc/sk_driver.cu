@@ -184,6 +184,8 @@ bool detect_stencil(const int64_t* rp, const int64_t* ci, const double* val, int
       }
       if (k != rp[i + 1]) ok = false;
     }
+    for (int sl = 0; sl < nslot && ok; ++sl)
+      if (!have[sl] || !std::isfinite(cval[sl])) ok = false;  // absent-neighbour zeros need finite values
     if (!ok) continue;
     out.dim = dim;
     out.g = g;

@@ -388,18 +388,40 @@ __device__ __forceinline__ void st_row(double* __restrict__ x, int64_t i, const 
   }
 }
 
-// Matrix-free stencil row of op * U (raw): all neighbours loaded unconditionally
-// (clamped addresses), absent ones skipped by selects -- exactly the CSR order.
-template <int S, int DIM>
-__device__ __forceinline__ void stencil_row(const SideConst& sc, const double* __restrict__ x, int64_t i,
+// Matrix-free stencil row of op * U (raw), 32-bit index arithmetic (device
+// n < 2^31). An absent neighbour is not loaded: its operand is +0.0, so its
+// term v*0 = +-0 leaves the running sum unchanged (the sum starts at +0.0 and
+// never becomes -0.0) -- bitwise the CSR gather that skips it, given finite
+// coefficients (enforced by the host-side detection).
+template <int S, int DIM, bool POW2 = false>
+__device__ __forceinline__ void stencil_row(const SideConst& sc, const double* __restrict__ x, int64_t i64,
                                             double* acc, double* own) {
   constexpr int K = DIM == 2 ? 5 : 7;
   constexpr int C = DIM == 2 ? 2 : 3;
-  int64_t ix, iy, iz;
-  grid_coords<S>(sc, i, ix, iy, iz);
-  const int64_t g = sc.sg, g2 = g * g;
+  const int i = (int)i64;
+  const int g = (int)sc.sg;
+  int ix, iy, iz = 0;
+  if (POW2) {
+    const int sh = sc.sg_pow2;
+    ix = i & (g - 1);
+    if (DIM == 2) {
+      iy = i >> sh;
+    } else {
+      iy = (i >> sh) & (g - 1);
+      iz = i >> (2 * sh);
+    }
+  } else {
+    const int r = i / g;
+    ix = i - r * g;
+    if (DIM == 2) {
+      iy = r;
+    } else {
+      iz = r / g;
+      iy = r - iz * g;
+    }
+  }
   bool pr[K];
-  int64_t col[K];
+  int col[K];
   if (DIM == 2) {
     pr[0] = iy > 0; col[0] = i - g;
     pr[1] = ix > 0; col[1] = i - 1;
@@ -407,6 +429,7 @@ __device__ __forceinline__ void stencil_row(const SideConst& sc, const double* _
     pr[3] = ix < g - 1; col[3] = i + 1;
     pr[4] = iy < g - 1; col[4] = i + g;
   } else {
+    const int g2 = g * g;
     pr[0] = iz > 0; col[0] = i - g2;
     pr[1] = iy > 0; col[1] = i - g;
     pr[2] = ix > 0; col[2] = i - 1;
@@ -417,33 +440,41 @@ __device__ __forceinline__ void stencil_row(const SideConst& sc, const double* _
   }
   double u[K][S];
 #pragma unroll
-  for (int k = 0; k < K; ++k) ld_raw<S>(x, pr[k] ? col[k] : i, u[k]);
+  for (int k = 0; k < K; ++k) {
+    if (pr[k]) {
+      ld_raw<S>(x, col[k], u[k]);
+    } else {
 #pragma unroll
-  for (int t = 0; t < S; ++t) {
-    acc[t] = 0.0;
-    own[t] = u[C][t];
+      for (int t = 0; t < S; ++t) u[k][t] = 0.0;
+    }
   }
 #pragma unroll
-  for (int k = 0; k < K; ++k) {
-    const double v = sc.scoef[k];
+  for (int t = 0; t < S; ++t) {
+    own[t] = u[C][t];
+    double a = 0.0;
 #pragma unroll
-    for (int t = 0; t < S; ++t) {
-      const double nv = __dadd_rn(acc[t], __dmul_rn(v, u[k][t]));
-      acc[t] = pr[k] ? nv : acc[t];
-    }
+    for (int k = 0; k < K; ++k) a = __dadd_rn(a, __dmul_rn(sc.scoef[k], u[k][t]));
+    acc[t] = a;
   }
 }
 
-// w row (normalised) and the raw own row of U_{k-1}
+// w row (normalised) and the raw own row of U_{k-1}. MODE: 0 CSR, 2/3 stencil
+// (general grid edge), 12/13 stencil with a power-of-two grid edge.
 template <int S, int MODE>
 __device__ __forceinline__ void w_row(const SideConst& sc, const double* __restrict__ x, const NF<S>& f,
                                       int64_t i, double* w, double* own) {
   double acc[S];
   if constexpr (MODE == 2 || MODE == 3)
-    stencil_row<S, MODE>(sc, x, i, acc, own);
+    stencil_row<S, MODE, false>(sc, x, i, acc, own);
+  else if constexpr (MODE == 12 || MODE == 13)
+    stencil_row<S, MODE - 10, true>(sc, x, i, acc, own);
   else
     raw_row_csr<S>(sc, x, i, acc, own);
   norm_row<S>(acc, f, w);
+}
+__device__ __forceinline__ int row_mode(const SideConst& sc) {
+  if (sc.sdim == 0) return 0;
+  return sc.sdim + (sc.sg_pow2 >= 0 ? 10 : 0);
 }
 
 // =====================================================================
@@ -466,12 +497,13 @@ __global__ void __launch_bounds__(256) k_spmm(SolveConst c) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
     double y[S], own[S];
-    if (sc.sdim == 2)
-      w_row<S, 2>(sc, x, f, i, y, own);
-    else if (sc.sdim == 3)
-      w_row<S, 3>(sc, x, f, i, y, own);
-    else
-      w_row<S, 0>(sc, x, f, i, y, own);
+    switch (row_mode(sc)) {
+      case 2: w_row<S, 2>(sc, x, f, i, y, own); break;
+      case 3: w_row<S, 3>(sc, x, f, i, y, own); break;
+      case 12: w_row<S, 12>(sc, x, f, i, y, own); break;
+      case 13: w_row<S, 13>(sc, x, f, i, y, own); break;
+      default: w_row<S, 0>(sc, x, f, i, y, own); break;
+    }
     st_row<S>(sc.w, i, y);
   }
 }
@@ -503,11 +535,21 @@ __device__ void final_tree(const double* part, int64_t P, double* out) {
     const int64_t grp = idx / NE;
     const int64_t p0 = grp * 32;
     const int cnt = (int)mn64(32, P - p0);
-    double a[32];
     if (cnt == 32) {
+      // tree over 32 = tree over four aligned tree-of-8 nodes (same canonical tree)
+      double node[4];
+#pragma unroll 1
+      for (int q = 0; q < 4; ++q) {
+        double a[8];
 #pragma unroll
-      for (int j = 0; j < 32; ++j) a[j] = __ldcg(part + (p0 + j) * NE + e);
-      gnode[e][grp] = tree32(a);
+        for (int j = 0; j < 8; ++j) a[j] = __ldcg(part + (p0 + 8 * q + j) * NE + e);
+#pragma unroll
+        for (int w = 4; w >= 1; w >>= 1)
+#pragma unroll
+          for (int j = 0; j < w; ++j) a[j] = __dadd_rn(a[2 * j], a[2 * j + 1]);
+        node[q] = a[0];
+      }
+      gnode[e][grp] = __dadd_rn(__dadd_rn(node[0], node[1]), __dadd_rn(node[2], node[3]));
     } else {
       gnode[e][grp] = tree_stream(part + p0 * NE + e, cnt, NE);
     }
@@ -664,28 +706,40 @@ __global__ void __launch_bounds__(256) k_gram(SolveConst c, int mode) {
 // Fused Lanczos passes (S <= 4). One warp per R1 segment, 8 warps per CTA
 // (the CTA node is the canonical tree's level-3 node).
 // =====================================================================
-template <int S, int MODE>
+template <int S, int MODE, bool TWO, bool CHECK>
 __device__ __forceinline__ void p1_body(const SideConst& sc, const double* __restrict__ u1, const NF<S>& f1,
-                                        const double* __restrict__ u0, bool two, int64_t base, int64_t n,
-                                        double* acc) {
+                                        const double* __restrict__ u0, int64_t base, int64_t n, double* acc) {
   constexpr int NB = S * S;
   const int lane = threadIdx.x & 31;
-#pragma unroll 4
+#pragma unroll
   for (int m = 0; m < kLRows; ++m) {
     const int64_t i = base + lane + 32 * m;
-    if (i < n) {
+    if (!CHECK || i < n) {
       double y[S], a1[S], a0[S];
       w_row<S, MODE>(sc, u1, f1, i, y, a1);
       if (MODE == 0) st_row<S>(sc.w, i, y);
-      if (two) ld_raw<S>(u0, i, a0);
+      if (TWO) ld_raw<S>(u0, i, a0);
 #pragma unroll
       for (int u = 0; u < S; ++u)
 #pragma unroll
         for (int t = 0; t < S; ++t) {
-          if (two) acc[u * S + t] = __dadd_rn(acc[u * S + t], __dmul_rn(a0[t], y[u]));
+          if (TWO) acc[u * S + t] = __dadd_rn(acc[u * S + t], __dmul_rn(a0[t], y[u]));
           acc[NB + u * S + t] = __dadd_rn(acc[NB + u * S + t], __dmul_rn(a1[t], y[u]));
         }
     }
+  }
+}
+template <int S, int MODE>
+__device__ __forceinline__ void p1_dispatch(const SideConst& sc, const double* __restrict__ u1, const NF<S>& f1,
+                                            const double* __restrict__ u0, bool two, int64_t base, int64_t n,
+                                            double* acc) {
+  const bool full = base + kSeg <= n;
+  if (two) {
+    if (full) p1_body<S, MODE, true, false>(sc, u1, f1, u0, base, n, acc);
+    else p1_body<S, MODE, true, true>(sc, u1, f1, u0, base, n, acc);
+  } else {
+    if (full) p1_body<S, MODE, false, false>(sc, u1, f1, u0, base, n, acc);
+    else p1_body<S, MODE, false, true>(sc, u1, f1, u0, base, n, acc);
   }
 }
 
@@ -710,8 +764,10 @@ __global__ void __launch_bounds__(256, 4) k_lanczos_p1(SolveConst c) {
   const bool two = k >= 2;
   const double* __restrict__ u1 = sc.blocks[k - 1];
   const double* __restrict__ u0 = two ? sc.blocks[k - 2] : u1;
-  NF<S> f1;
-  load_nf<S>(sc.nfac, k - 1, f1);
+  __shared__ NF<S> f1s;
+  if (threadIdx.x == 0) load_nf<S>(sc.nfac, k - 1, f1s);
+  __syncthreads();
+  const NF<S>& f1 = f1s;
   const int warp = threadIdx.x >> 5;
   const int64_t seg = cta * kFusedSegsPerCta + warp;
   const int nvalid_cta = (int)mn64(kFusedSegsPerCta, nseg - cta * kFusedSegsPerCta);
@@ -720,12 +776,13 @@ __global__ void __launch_bounds__(256, 4) k_lanczos_p1(SolveConst c) {
   for (int e = 0; e < NE; ++e) acc[e] = 0.0;
   if (seg < nseg) {
     const int64_t base = seg * kSeg;
-    if (sc.sdim == 2)
-      p1_body<S, 2>(sc, u1, f1, u0, two, base, sc.n, acc);
-    else if (sc.sdim == 3)
-      p1_body<S, 3>(sc, u1, f1, u0, two, base, sc.n, acc);
-    else
-      p1_body<S, 0>(sc, u1, f1, u0, two, base, sc.n, acc);
+    switch (row_mode(sc)) {
+      case 2: p1_dispatch<S, 2>(sc, u1, f1, u0, two, base, sc.n, acc); break;
+      case 3: p1_dispatch<S, 3>(sc, u1, f1, u0, two, base, sc.n, acc); break;
+      case 12: p1_dispatch<S, 12>(sc, u1, f1, u0, two, base, sc.n, acc); break;
+      case 13: p1_dispatch<S, 13>(sc, u1, f1, u0, two, base, sc.n, acc); break;
+      default: p1_dispatch<S, 0>(sc, u1, f1, u0, two, base, sc.n, acc); break;
+    }
   }
   warp_seg_to_cta<NE>(acc, nvalid_cta, sc.part + cta * NE);
   if (!last_cta_arrive(sc.counter + 0, (unsigned)ncta)) return;
@@ -745,16 +802,15 @@ __global__ void __launch_bounds__(256, 4) k_lanczos_p1(SolveConst c) {
   }
 }
 
-template <int S, int MODE>
+template <int S, int MODE, bool TWO, bool CHECK>
 __device__ __forceinline__ void p2_body(const SideConst& sc, const double* __restrict__ u1, const NF<S>& f1,
-                                        const double* __restrict__ u0, bool two, const double* m1,
-                                        const double* m0, double* __restrict__ out, int64_t base, int64_t n,
-                                        double* acc) {
+                                        const double* __restrict__ u0, const double* m1, const double* m0,
+                                        double* __restrict__ out, int64_t base, int64_t n, double* acc) {
   const int lane = threadIdx.x & 31;
-#pragma unroll 4
+#pragma unroll
   for (int m = 0; m < kLRows; ++m) {
     const int64_t i = base + lane + 32 * m;
-    if (i < n) {
+    if (!CHECK || i < n) {
       double y[S], a1[S], a0[S];
       if (MODE == 0) {
         ld_raw_cg<S>(sc.w, i, y);
@@ -762,7 +818,7 @@ __device__ __forceinline__ void p2_body(const SideConst& sc, const double* __res
       } else {
         w_row<S, MODE>(sc, u1, f1, i, y, a1);
       }
-      if (two) {
+      if (TWO) {
         ld_raw<S>(u0, i, a0);
 #pragma unroll
         for (int u = 0; u < S; ++u) {
@@ -791,11 +847,25 @@ __device__ __forceinline__ void p2_body(const SideConst& sc, const double* __res
     }
   }
 }
+template <int S, int MODE>
+__device__ __forceinline__ void p2_dispatch(const SideConst& sc, const double* __restrict__ u1, const NF<S>& f1,
+                                            const double* __restrict__ u0, bool two, const double* m1,
+                                            const double* m0, double* __restrict__ out, int64_t base, int64_t n,
+                                            double* acc) {
+  const bool full = base + kSeg <= n;
+  if (two) {
+    if (full) p2_body<S, MODE, true, false>(sc, u1, f1, u0, m1, m0, out, base, n, acc);
+    else p2_body<S, MODE, true, true>(sc, u1, f1, u0, m1, m0, out, base, n, acc);
+  } else {
+    if (full) p2_body<S, MODE, false, false>(sc, u1, f1, u0, m1, m0, out, base, n, acc);
+    else p2_body<S, MODE, false, true>(sc, u1, f1, u0, m1, m0, out, base, n, acc);
+  }
+}
 
 // Lanczos pass 2: U_k = w - U_{k-2} M_{k-2} - U_{k-1} M_{k-1} (+ R1 self Gram,
 // finalise). Matrix-free operators recompute w from U_{k-1} instead of reading it.
 template <int S>
-__global__ void __launch_bounds__(256, 4) k_lanczos_p2(SolveConst c) {
+__global__ void __launch_bounds__(256, 5) k_lanczos_p2(SolveConst c) {
   constexpr int NS = S * (S + 1) / 2;
   const int side = blockIdx.z;
   if (side >= c.nsides) return;
@@ -812,14 +882,15 @@ __global__ void __launch_bounds__(256, 4) k_lanczos_p2(SolveConst c) {
   const bool two = k >= 2;
   const double* __restrict__ u1 = sc.blocks[k - 1];
   const double* __restrict__ u0 = two ? sc.blocks[k - 2] : u1;
-  NF<S> f1;
-  load_nf<S>(sc.nfac, k - 1, f1);
-  double m1[S * S], m0[S * S];
-#pragma unroll
-  for (int e = 0; e < S * S; ++e) {
-    m1[e] = __ldcg(sc.mcoef + (k - 1) * S * S + e);
-    m0[e] = two ? __ldcg(sc.mcoef + (k - 2) * S * S + e) : 0.0;
+  __shared__ NF<S> f1s;
+  __shared__ double m1[S * S], m0[S * S];
+  if (threadIdx.x == 0) load_nf<S>(sc.nfac, k - 1, f1s);
+  if (threadIdx.x < S * S) {
+    m1[threadIdx.x] = __ldcg(sc.mcoef + (k - 1) * S * S + threadIdx.x);
+    m0[threadIdx.x] = two ? __ldcg(sc.mcoef + (k - 2) * S * S + threadIdx.x) : 0.0;
   }
+  __syncthreads();
+  const NF<S>& f1 = f1s;
   double* __restrict__ out = sc.blocks[k];
   const int warp = threadIdx.x >> 5;
   const int64_t seg = cta * kFusedSegsPerCta + warp;
@@ -829,12 +900,13 @@ __global__ void __launch_bounds__(256, 4) k_lanczos_p2(SolveConst c) {
   for (int e = 0; e < NS; ++e) acc[e] = 0.0;
   if (seg < nseg) {
     const int64_t base = seg * kSeg;
-    if (sc.sdim == 2)
-      p2_body<S, 2>(sc, u1, f1, u0, two, m1, m0, out, base, sc.n, acc);
-    else if (sc.sdim == 3)
-      p2_body<S, 3>(sc, u1, f1, u0, two, m1, m0, out, base, sc.n, acc);
-    else
-      p2_body<S, 0>(sc, u1, f1, u0, two, m1, m0, out, base, sc.n, acc);
+    switch (row_mode(sc)) {
+      case 2: p2_dispatch<S, 2>(sc, u1, f1, u0, two, m1, m0, out, base, sc.n, acc); break;
+      case 3: p2_dispatch<S, 3>(sc, u1, f1, u0, two, m1, m0, out, base, sc.n, acc); break;
+      case 12: p2_dispatch<S, 12>(sc, u1, f1, u0, two, m1, m0, out, base, sc.n, acc); break;
+      case 13: p2_dispatch<S, 13>(sc, u1, f1, u0, two, m1, m0, out, base, sc.n, acc); break;
+      default: p2_dispatch<S, 0>(sc, u1, f1, u0, two, m1, m0, out, base, sc.n, acc); break;
+    }
   }
   warp_seg_to_cta<NS>(acc, nvalid_cta, sc.part + cta * NS);
   if (!last_cta_arrive(sc.counter + 1, (unsigned)ncta)) return;
