@@ -8,6 +8,6 @@ $CMD > gpurun_out/plain_$TAG.log 2>&1 && \
 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -c 300 --csv \
     --log-file gpurun_out/launches_$TAG.csv $CMD > gpurun_out/ncu_launch_$TAG.log 2>&1
 echo launches_rc=$?
-ncu --set full --clock-control none --import-source on -k regex:"k_update|k_gram|k_spmm" -s 60 -c 3 \
+ncu --set full --clock-control none --import-source on -k regex:"k_lanczos_p|k_cg_b" -s 60 -c 3 \
     -o gpurun_out/prof_$TAG $CMD > gpurun_out/ncu_full_$TAG.log 2>&1
 echo full_rc=$?
