@@ -60,7 +60,10 @@ struct DevState {
   int64_t rows_x, cols_x;  // shape of the iterate core
   int64_t rows_q, cols_q;  // shape of the image window of this iteration
   double rho, alpha, beta, omega, norm_r0, norm_shadow, denom;
-  int64_t rows_s, cols_s;  // BiCGSTAB: shape of S
+  int64_t rows_s, cols_s;  // BiCGSTAB: shape of S (= Q's shape)
+  int64_t rows_t, cols_t;  // BiCGSTAB: shape of T (= the next residual's shape)
+  double tt, ss, st;       // BiCGSTAB reductions
+  int64_t rows_po, cols_po;  // BiCGSTAB: shape of the previous direction core
   SideState side[2];
 };
 
@@ -75,8 +78,9 @@ struct SideConst {
   double* wx;                // scratch n x s: CGS2 intermediate / transposed start block
   double* qh;                // scratch n x s: Householder Q
   double* hw;                // scratch n x s: Householder work copy
-  double* hband;             // Lanczos H bands [cap_steps][3][s*s] | Arnoldi dense H
-  int64_t hld;               // Arnoldi: leading dimension of the dense H
+  double* hband;             // Lanczos H bands [cap_steps][3][s*s] | Arnoldi packed H:
+                             // column block e has (e+2)s rows at offset s^2 e(e+3)/2
+  int64_t hld;               // unused
   double* nfac;              // [cap_blocks][s*s + s] normalisation factor N_b and 1/diag
   double* coef;              // [cap_blocks][s*s] CGS coefficients (pass 1)
   double* coef2;             // [cap_blocks][s*s] second-pass coefficients

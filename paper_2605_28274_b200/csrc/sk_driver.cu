@@ -303,6 +303,8 @@ struct Solver {
   // cores
   int64_t rcap = 0;
   double *X = nullptr, *R = nullptr, *P0 = nullptr, *P1 = nullptr, *cpart = nullptr;
+  double *Qc = nullptr, *Sc = nullptr, *Tc = nullptr, *Rs = nullptr;
+  int64_t hcap_steps = 0;  // Arnoldi packed-H capacity (steps)
   unsigned int* ccounter = nullptr;
   double *hist_rel = nullptr, *hist_tk = nullptr, *hist_tb = nullptr;
   sk::DevState* dstate = nullptr;
@@ -464,13 +466,18 @@ struct Solver {
     c.hist_tk = hist_tk;
     c.hist_tb = hist_tb;
     c.st = dstate;
-    grow_cores(std::min<int64_t>((max_iter + 2) * s, 512));
+    if (arnoldi) {
+      Rs = dalloc<double>(s * s);
+      c.Rs = Rs;
+      ensure_hcap(std::min<int64_t>(cap_blocks, 64));
+    }
+    grow_cores(std::min<int64_t>((arnoldi ? 2 * max_iter + 3 : max_iter + 2) * s, 512));
   }
 
   void grow_cores(int64_t need) {
     if (need <= rcap) return;
     int64_t ncap = std::max<int64_t>(need, 2 * rcap);
-    ncap = std::min<int64_t>(ncap, ((max_iter + 2) * s + 31) / 32 * 32 + 32);
+    ncap = std::min<int64_t>(ncap, (cap_blocks * s + 31) / 32 * 32 + 32);
     ncap = std::max<int64_t>(ncap, need);
     ncap = (ncap + 31) / 32 * 32;
     auto grow = [&](double*& buf) {
@@ -485,20 +492,48 @@ struct Solver {
     grow(X);
     grow(R);
     grow(P0);
-    grow(P1);
+    if (!arnoldi) grow(P1);
+    if (arnoldi) {
+      grow(Qc);
+      grow(Sc);
+      grow(Tc);
+    }
     dfree(cpart);
     dfree(ccounter);
     const int64_t nt = ncap / 32;
-    cpart = dalloc<double>(nt * nt + nt + 64);
+    cpart = dalloc<double>(3 * nt * nt + nt + 1024);
     ccounter = dalloc<unsigned int>(8);
     rcap = ncap;
     c.X = X;
     c.R = R;
     c.P[0] = P0;
     c.P[1] = P1;
+    c.Q = Qc;
+    c.S = Sc;
+    c.T = Tc;
     c.ld = rcap;
     c.cpart = cpart;
     c.ccounter = ccounter;
+  }
+
+  // packed upper block Hessenberg: column block e has (e+2)s rows at s^2 e(e+3)/2
+  static int64_t hpacked_size(int64_t steps, int64_t s) { return s * s * (steps * (steps + 3) / 2); }
+  void ensure_hcap(int64_t steps) {
+    if (!arnoldi || steps <= hcap_steps) return;
+    int64_t ncap = std::max<int64_t>(steps, 2 * hcap_steps);
+    ncap = std::max<int64_t>(std::min<int64_t>(ncap, cap_blocks), steps);
+    for (int sd = 0; sd < nsides; ++sd) {
+      SideBuf& b = side[sd];
+      double* nh = dalloc<double>(hpacked_size(ncap, s));
+      if (b.hband) {
+        CK(cudaMemcpyAsync(nh, b.hband, sizeof(double) * hpacked_size(hcap_steps, s), cudaMemcpyDeviceToDevice, st));
+        dfree(b.hband);
+      }
+      b.hband = nh;
+      c.side[sd].hband = nh;
+    }
+    if (nsides == 1) c.side[1] = c.side[0];
+    hcap_steps = ncap;
   }
 
   void ensure_blocks(int sd, int64_t need) {
@@ -543,6 +578,12 @@ struct Solver {
     for (int sd = 0; sd < nsides; ++sd) b += 8.0 * P.op[sd].n * s * (J + 1 + (P.op[sd].stencil.dim ? 0 : 1));
     return b;
   }
+  // Arnoldi CGS2 extension with kb prior blocks (12nnz + 4(n+1) + 8ns(3kb+5))
+  double arnoldi_bytes(int64_t kb) const {
+    double b = 0;
+    for (int sd = 0; sd < nsides; ++sd) b += csr_bytes(sd) + 8.0 * P.op[sd].n * s * (3.0 * kb + 5.0);
+    return b;
+  }
   double pass_bytes(int64_t k, int extra) const {
     const double J = (double)std::min<int64_t>(k + 1, 2);
     double b = 0;
@@ -580,6 +621,20 @@ struct Solver {
     std::vector<std::vector<double>> caps;
     std::vector<std::pair<int64_t, int64_t>> cap_shape;
     for (int64_t k = 0; k < max_iter && !done; ++k) {
+      if (arnoldi) {
+        for (int sd = 0; sd < nsides; ++sd) ensure_blocks(sd, 2 * k + 3);
+        ensure_hcap(2 * k + 2);
+        grow_cores((2 * k + 3) * s);
+        const double r1 = (double)((2 * k + 2) * s), r2 = (double)((2 * k + 3) * s);
+        timed(6, arnoldi_bytes(2 * k + 1), [&] { sk::launch_arnoldi_ext(c, 2 * k + 1, st); });
+        dbg("arnoldi1", k);
+        timed(7, 2.0 * r1 * r1 * r1, [&] { sk::launch_bicgstab_half(c, 0, (2 * k + 2) * s, st); });
+        dbg("half1", k);
+        timed(6, arnoldi_bytes(2 * k + 2), [&] { sk::launch_arnoldi_ext(c, 2 * k + 2, st); });
+        dbg("arnoldi2", k);
+        timed(7, 2.0 * r2 * r2 * r2, [&] { sk::launch_bicgstab_half(c, 1, (2 * k + 3) * s, st); });
+        dbg("half2", k);
+      } else {
       for (int sd = 0; sd < nsides; ++sd) ensure_blocks(sd, k + 2);
       grow_cores((k + 2) * s);
       const double rp = (double)((k + 1) * s), rq = (double)((k + 2) * s);
@@ -602,6 +657,7 @@ struct Solver {
       dbg("core_a", k);
       timed(5, 8.0 * (4 * rp * rp + rq * rq), [&] { sk::launch_cg_b(c, (k + 2) * s, st); });
       dbg("core_b", k);
+      }
       CK(cudaMemcpyAsync(&hstat[k % RING], &dstate->status, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
       CK(cudaEventRecord(rev[k % RING], st));
       enq = k + 1;
@@ -725,6 +781,10 @@ struct Solver {
     dfree(R);
     dfree(P0);
     dfree(P1);
+    dfree(Qc);
+    dfree(Sc);
+    dfree(Tc);
+    dfree(Rs);
     dfree(cpart);
     dfree(ccounter);
     dfree(hist_rel);
@@ -910,8 +970,6 @@ sk_status sk_problem_solve(sk_problem* p, const sk_config* cfg, sk_solution** ou
   if (out) *out = nullptr;
   return run_guarded([&] {
     if (!p) throw SkError(SK_ERR_DIMENSION, "null problem");
-    if (p->method == SK_METHOD_BICGSTAB)
-      throw SkError(SK_ERR_UNSUPPORTED, "factorized_bicgstab: device path not built yet");
     CK(cudaSetDevice(p->device));
     Solver solver(*p, default_cfg(cfg));
     *out = solver.run();

@@ -73,8 +73,10 @@ __device__ inline int64_t first_block(const SolveConst& c, int64_t k) {
 __device__ inline double* hb_ptr(const SideConst& sc, int64_t e, int d, int s) {
   return sc.hband + (e * 3 + d) * (int64_t)(s * s);
 }
+// packed upper block Hessenberg (Arnoldi): column block e has (e+2)s rows
+__device__ __forceinline__ int64_t hcol_off(int64_t e, int s) { return (int64_t)s * s * (e * (e + 3) / 2); }
 __device__ inline double* hcol_ptr(const SideConst& sc, int64_t e, int cc, int s) {
-  return sc.hband + (e * s + cc) * sc.hld;
+  return sc.hband + hcol_off(e, s) + (int64_t)cc * (e + 2) * s;
 }
 
 // coeff2 in the reference loop order (block_krylov.cpp:105-108)
@@ -1709,6 +1711,335 @@ template struct Launch<SK_INST_S>;
 #endif
 
 #ifdef SK_INST_COMMON
+// =====================================================================
+// BiCGSTAB (factorized_solvers.cpp:220-389) on the device
+// =====================================================================
+__device__ __forceinline__ double hpacked(const double* hb, int s, int64_t i, int64_t l) {
+  const int64_t e = l / s;
+  const int64_t hr = (e + 2) * s;
+  if (i >= hr) return 0.0;
+  return hb[hcol_off(e, s) + (l % s) * hr + i];
+}
+
+// Dense core image with the upper block Hessenberg H (V side) and G (W side):
+// q(i,j) = Hpart(i,j) [j < pc] + Gpart(i,j) [i < pr], each part an fma chain over
+// the contraction index in ascending order (oracle image(), Arnoldi branch).
+// Leading structural zeros are skipped per tile; fma(0, x, acc) = acc for the
+// zero padding inside a tile (acc never -0, finite operands).
+constexpr int kImT = 64, kImK = 16;
+__global__ void __launch_bounds__(256) k_bi_image(SolveConst c, int which) {
+  DevState* st = c.st;
+  if (st->status != RUNNING) return;
+  const int s = c.s;
+  const double* src = which == 0 ? c.P[0] : c.S;
+  double* dst = which == 0 ? c.Q : c.T;
+  const int64_t pr = which == 0 ? st->rows_p : st->rows_s, pc = which == 0 ? st->cols_p : st->cols_s;
+  const int64_t ro = which == 0 ? st->rows_q : st->rows_t, co = which == 0 ? st->cols_q : st->cols_t;
+  const int64_t i0 = (int64_t)blockIdx.x * kImT, j0 = (int64_t)blockIdx.y * kImT;
+  if (i0 >= ro || j0 >= co) return;
+  const double* hv = c.side[0].hband;
+  const double* hw = c.side[c.nsides > 1 ? 1 : 0].hband;
+  __shared__ double As[kImK][kImT + 1], Bs[kImK][kImT + 1];
+  const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
+  double accH[4][4], accG[4][4];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) accH[a][b] = accG[a][b] = 0.0;
+  const int64_t ld = c.ld;
+  // H part: rows i (H rows), columns j < pc, contraction l in [lH0, pr)
+  if (j0 < pc) {
+    const int64_t lH0 = (int64_t)s * mx64(0, i0 / s - 1);
+    for (int64_t l0 = lH0; l0 < pr; l0 += kImK) {
+      for (int idx = threadIdx.x; idx < kImK * kImT; idx += blockDim.x) {
+        const int kk = idx / kImT, ii = idx % kImT;
+        const int64_t l = l0 + kk;
+        As[kk][ii] = (l < pr && i0 + ii < ro) ? hpacked(hv, s, i0 + ii, l) : 0.0;
+        Bs[kk][ii] = (l < pr && j0 + ii < pc) ? src[(j0 + ii) * ld + l] : 0.0;
+      }
+      __syncthreads();
+#pragma unroll
+      for (int kk = 0; kk < kImK; ++kk) {
+        double av[4], bv[4];
+#pragma unroll
+        for (int a = 0; a < 4; ++a) av[a] = As[kk][ty * 4 + a];
+#pragma unroll
+        for (int b = 0; b < 4; ++b) bv[b] = Bs[kk][tx * 4 + b];
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+          for (int b = 0; b < 4; ++b) accH[a][b] = __fma_rn(av[a], bv[b], accH[a][b]);
+      }
+      __syncthreads();
+    }
+  }
+  // G part: rows i < pr, columns j (G rows), contraction l in [lG0, pc)
+  if (i0 < pr) {
+    const int64_t lG0 = (int64_t)s * mx64(0, j0 / s - 1);
+    for (int64_t l0 = lG0; l0 < pc; l0 += kImK) {
+      for (int idx = threadIdx.x; idx < kImK * kImT; idx += blockDim.x) {
+        const int kk = idx / kImT, ii = idx % kImT;
+        const int64_t l = l0 + kk;
+        As[kk][ii] = (l < pc && i0 + ii < pr) ? src[l * ld + i0 + ii] : 0.0;
+        Bs[kk][ii] = (l < pc && j0 + ii < co) ? hpacked(hw, s, j0 + ii, l) : 0.0;
+      }
+      __syncthreads();
+#pragma unroll
+      for (int kk = 0; kk < kImK; ++kk) {
+        double av[4], bv[4];
+#pragma unroll
+        for (int a = 0; a < 4; ++a) av[a] = As[kk][ty * 4 + a];
+#pragma unroll
+        for (int b = 0; b < 4; ++b) bv[b] = Bs[kk][tx * 4 + b];
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+          for (int b = 0; b < 4; ++b) accG[a][b] = __fma_rn(av[a], bv[b], accG[a][b]);
+      }
+      __syncthreads();
+    }
+  }
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      const int64_t i = i0 + ty * 4 + a, j = j0 + tx * 4 + b;
+      if (i >= ro || j >= co) continue;
+      const bool hj = j < pc, gi = i < pr;
+      const double q = (hj && gi) ? __dadd_rn(accH[a][b], accG[a][b]) : (hj ? accH[a][b] : (gi ? accG[a][b] : 0.0));
+      dst[j * ld + i] = q;
+    }
+}
+
+__device__ inline void bi_breakdown(const SolveConst& c) {
+  DevState* st = c.st;
+  st->status = BREAKDOWN;
+  c.hist_rel[st->k + 1] = c.hist_rel[st->k];
+  c.hist_tb[st->k + 1] = (double)globaltimer();
+  if (c.hist_tk[st->k + 1] == 0.0) c.hist_tk[st->k + 1] = c.hist_tb[st->k + 1];
+  st->nrec = st->k + 2;
+}
+
+// after an extension pair: breakdown check and the image window (sched = (2k+2+which)s)
+__global__ void k_bi_begin(SolveConst c, int which) {
+  DevState* st = c.st;
+  if (threadIdx.x != 0 || st->status != RUNNING) return;
+  if (any_side_broken(c)) {
+    bi_breakdown(c);
+    return;
+  }
+  const int s = c.s;
+  const int64_t k = st->k;
+  const int64_t sched = (2 * k + 2 + which) * s;
+  const int64_t vc = st->side[0].blocks * s, wc = st->side[c.nsides > 1 ? 1 : 0].blocks * s;
+  const int64_t r = sched < vc ? sched : vc, cc = sched < wc ? sched : wc;
+  if (which == 0) {
+    st->rows_q = r;
+    st->cols_q = cc;
+    c.hist_tk[k + 1] = (double)globaltimer();  // first extension done
+  } else {
+    st->rows_t = r;
+    st->cols_t = cc;
+  }
+}
+
+// R2 contract over an s x s window (one tile): lane i sums its row, butterfly
+__device__ __forceinline__ double r2_small(const double* a, int64_t lda, const double* b, int64_t ldb, int s) {
+  const int lane = threadIdx.x & 31;
+  double acc = 0.0;
+  if (lane < s)
+    for (int j = 0; j < s; ++j) acc = __dadd_rn(acc, __dmul_rn(a[j * lda + lane], b[j * ldb + lane]));
+  return butterfly(acc);
+}
+
+// denom = <R~0, Q>_{s x s}, guard on the angle, alpha (factorized_solvers.cpp:292-300)
+__global__ void k_bi_alpha(SolveConst c) {
+  DevState* st = c.st;
+  if (st->status != RUNNING) return;
+  const int s = c.s;
+  const double denom = r2_small(c.Rs, s, c.Q, c.ld, s);
+  const double qw2 = r2_small(c.Q, c.ld, c.Q, c.ld, s);
+  if (threadIdx.x != 0) return;
+  const double q_win = __dsqrt_rn(qw2);
+  st->denom = denom;
+  if (fabs(denom) < __dmul_rn(__dmul_rn(c.tol, st->norm_shadow), q_win)) {
+    bi_breakdown(c);
+    return;
+  }
+  st->alpha = __ddiv_rn(st->rho, denom);
+  st->rows_s = st->rows_q;
+  st->cols_s = st->cols_q;
+}
+
+// S = embed(R) - alpha Q over Q's window (factorized_solvers.cpp:301-302)
+__global__ void k_bi_s(SolveConst c) {
+  DevState* st = c.st;
+  if (st->status != RUNNING) return;
+  const int64_t rq = st->rows_q, cq = st->cols_q, rp = st->rows_p, cp = st->cols_p;
+  const double na = -st->alpha;
+  const int64_t total = rq * cq;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t j = idx / rq, i = idx - j * rq;
+    const int64_t o = j * c.ld + i;
+    const double r = (i < rp && j < cp) ? c.R[o] : 0.0;
+    c.S[o] = __dadd_rn(r, __dmul_rn(na, c.Q[o]));
+  }
+}
+
+// tt = <T,T>, ss = <S,S>, st = <S,T>_S (R2 over their windows), omega (:320-336)
+__global__ void __launch_bounds__(256) k_bi_omega(SolveConst c) {
+  DevState* st = c.st;
+  if (st->status != RUNNING) return;
+  const int64_t rt = st->rows_t, ct = st->cols_t, rs = st->rows_s, cs = st->cols_s;
+  const int64_t nti = (rt + kTile - 1) / kTile, ntj = (ct + kTile - 1) / kTile;
+  const int64_t sti = (rs + kTile - 1) / kTile, stj = (cs + kTile - 1) / kTile;
+  const int64_t ti = blockIdx.x, tj = blockIdx.y;
+  if (ti >= nti || tj >= ntj) return;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (warp == 0) {
+    const int64_t i = ti * kTile + lane;
+    double att = 0.0, ass = 0.0, ast = 0.0;
+    if (i < rt)
+      for (int q = 0; q < kTile; ++q) {
+        const int64_t j = tj * kTile + q;
+        if (j >= ct) break;
+        const double t = c.T[j * c.ld + i];
+        att = __dadd_rn(att, __dmul_rn(t, t));
+        if (i < rs && j < cs) {
+          const double sv = c.S[j * c.ld + i];
+          ass = __dadd_rn(ass, __dmul_rn(sv, sv));
+          ast = __dadd_rn(ast, __dmul_rn(sv, t));
+        }
+      }
+    att = butterfly(att);
+    ass = butterfly(ass);
+    ast = butterfly(ast);
+    if (lane == 0) {
+      c.cpart[tj * nti + ti] = att;
+      if (ti < sti && tj < stj) {
+        const int64_t base = nti * ntj + 256;
+        c.cpart[base + tj * sti + ti] = ass;
+        c.cpart[base + sti * stj + tj * sti + ti] = ast;
+      }
+    }
+  }
+  if (!last_cta_arrive(c.ccounter, (unsigned)(nti * ntj))) return;
+  __shared__ double scratch[256];
+  const int64_t base = nti * ntj + 256;
+  double* scr = ntj <= 256 ? scratch : c.cpart + base + 2 * sti * stj;
+  const double tt = r2_final(c.cpart, nti, ntj, scr);
+  double* scr2 = stj <= 256 ? scratch : c.cpart + base + 2 * sti * stj;
+  const double ss = r2_final(c.cpart + base, sti, stj, scr2);
+  const double stv = r2_final(c.cpart + base + sti * stj, sti, stj, scr2);
+  if (threadIdx.x != 0) return;
+  st->tt = tt;
+  st->ss = ss;
+  st->st = stv;
+  if (__dsqrt_rn(ss) <= __dmul_rn(c.eps, st->norm_r0)) {
+    st->omega = 0.0;  // converged at the half step
+  } else if (tt < __dmul_rn(c.tol, ss)) {
+    bi_breakdown(c);
+  } else {
+    st->omega = __ddiv_rn(stv, tt);
+  }
+}
+
+// X = (embed(X) + alpha embed(P)) + omega S; R = embed(S) - omega T; ||R||; rho',
+// angle guard, beta (factorized_solvers.cpp:338-367)
+__global__ void __launch_bounds__(256) k_bi_update(SolveConst c) {
+  DevState* st = c.st;
+  if (st->status != RUNNING) return;
+  const int64_t rt = st->rows_t, ct = st->cols_t, rs = st->rows_s, cs = st->cols_s;
+  const int64_t rp = st->rows_p, cp = st->cols_p;
+  const int64_t nti = (rt + kTile - 1) / kTile, ntj = (ct + kTile - 1) / kTile;
+  const int64_t ti = blockIdx.x, tj = blockIdx.y;
+  if (ti >= nti || tj >= ntj) return;
+  const double alpha = st->alpha, omega = st->omega, nom = -omega;
+  __shared__ double f[kTile * kTile];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t i = ti * kTile + lane;
+  for (int q = 0; q < 4; ++q) {
+    const int lc = warp * 4 + q;
+    const int64_t j = tj * kTile + lc;
+    double fv = 0.0;
+    if (i < rt && j < ct) {
+      const int64_t o = j * c.ld + i;
+      const bool ins = i < rs && j < cs;
+      const double sv = ins ? c.S[o] : 0.0;
+      if (ins) {
+        const double pv = (i < rp && j < cp) ? c.P[0][o] : 0.0;
+        c.X[o] = __dadd_rn(__dadd_rn(c.X[o], __dmul_rn(alpha, pv)), __dmul_rn(omega, sv));
+      }
+      const double rn = __dadd_rn(sv, __dmul_rn(nom, c.T[o]));
+      c.R[o] = rn;
+      fv = __dmul_rn(rn, rn);
+    }
+    f[lc * kTile + lane] = fv;
+  }
+  __syncthreads();
+  if (warp == 0) {
+    const int nr = (int)mn64(kTile, rt - ti * kTile), nc = (int)mn64(kTile, ct - tj * kTile);
+    const double v = tile_reduce(f, nr, nc);
+    if (lane == 0) c.cpart[tj * nti + ti] = v;
+  }
+  if (!last_cta_arrive(c.ccounter, (unsigned)(nti * ntj))) return;
+  __shared__ double scratch[256];
+  double* scr = ntj <= 256 ? scratch : c.cpart + nti * ntj;
+  const double rr = r2_final(c.cpart, nti, ntj, scr);
+  const int s = c.s;
+  double rho_next = 0.0, rw2 = 0.0;
+  if (threadIdx.x < 32) {
+    rho_next = r2_small(c.Rs, s, c.R, c.ld, s);
+    rw2 = r2_small(c.R, c.ld, c.R, c.ld, s);
+  }
+  if (threadIdx.x != 0) return;
+  const int64_t k = st->k;
+  const double norm_r = __dsqrt_rn(rr);
+  c.hist_rel[k + 1] = __ddiv_rn(norm_r, st->norm_r0);
+  c.hist_tb[k + 1] = (double)globaltimer();
+  st->nrec = k + 2;
+  st->rows_x = rs;
+  st->cols_x = cs;
+  st->rows_po = rp;
+  st->cols_po = cp;
+  st->rows_p = rt;
+  st->cols_p = ct;
+  st->k = k + 1;
+  if (norm_r <= __dmul_rn(st->norm_r0, c.eps)) {
+    st->status = CONVERGED;
+    return;
+  }
+  const double r_win = __dsqrt_rn(rw2);
+  if (fabs(rho_next) < __dmul_rn(__dmul_rn(c.tol, st->norm_shadow), r_win)) {
+    st->status = BREAKDOWN;  // record already written for this iteration
+    return;
+  }
+  st->beta = __dmul_rn(__ddiv_rn(alpha, omega), __ddiv_rn(rho_next, st->rho));
+  st->rho = rho_next;
+  if (st->k >= c.max_iter) st->status = MAXITER;
+}
+
+// P = (R + beta embed(P)) + (-beta*omega) embed(Q) over R's window (:369-375)
+__global__ void k_bi_p(SolveConst c) {
+  DevState* st = c.st;
+  if (st->status != RUNNING) return;
+  const int64_t rt = st->rows_p, ct = st->cols_p, rp = st->rows_po, cp = st->cols_po;
+  const int64_t rq = st->rows_q, cq = st->cols_q;
+  const double beta = st->beta, nbo = __dmul_rn(-beta, st->omega);
+  const int64_t total = rt * ct;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t j = idx / rt, i = idx - j * rt;
+    const int64_t o = j * c.ld + i;
+    const double pv = (i < rp && j < cp) ? c.P[0][o] : 0.0;
+    const double qv = (i < rq && j < cq) ? c.Q[o] : 0.0;
+    c.P[0][o] = __dadd_rn(__dadd_rn(c.R[o], __dmul_rn(beta, pv)), __dmul_rn(nbo, qv));
+  }
+}
+#endif
+
+#ifdef SK_INST_COMMON
 static int g_launches = 0;
 int launch_count() { return g_launches; }
 void launch_count_reset() { g_launches = 0; }
@@ -1775,6 +2106,21 @@ void launch_arnoldi_ext(const SolveConst& c, int64_t kmax_blocks, cudaStream_t s
   SK_DISPATCH_S(c.s, update(c, (int)UM_SECOND, st));
   SK_DISPATCH_S(c.s, householder(c, 0, st));
   g_launches += 6;
+}
+void launch_bicgstab_half(const SolveConst& c, int which, int64_t rmax, cudaStream_t st) {
+  k_bi_begin<<<1, 32, 0, st>>>(c, which);
+  const unsigned nt = (unsigned)((rmax + kImT - 1) / kImT);
+  k_bi_image<<<dim3(nt, nt), 256, 0, st>>>(c, which);
+  if (which == 0) {
+    k_bi_alpha<<<1, 32, 0, st>>>(c);
+    k_bi_s<<<rows_grid(rmax * rmax), 256, 0, st>>>(c);
+  } else {
+    const unsigned tt = (unsigned)((rmax + kTile - 1) / kTile);
+    k_bi_omega<<<dim3(tt, tt), 256, 0, st>>>(c);
+    k_bi_update<<<dim3(tt, tt), 256, 0, st>>>(c);
+    k_bi_p<<<rows_grid(rmax * rmax), 256, 0, st>>>(c);
+  }
+  g_launches += which == 0 ? 4 : 5;
 }
 void launch_cg_a(const SolveConst& c, int64_t rmax, cudaStream_t st) {
   SK_DISPATCH_S(c.s, cg_a(c, rmax, st));

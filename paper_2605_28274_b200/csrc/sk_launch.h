@@ -18,6 +18,7 @@ void launch_rare(const SolveConst& c, int64_t kmax_blocks, cudaStream_t st);
 void launch_arnoldi_ext(const SolveConst& c, int64_t kmax_blocks, cudaStream_t st);
 void launch_export_block(int s, const double* blk, const double* nfac, int64_t b, double* out,
                          int64_t n, cudaStream_t st);
+void launch_bicgstab_half(const SolveConst& c, int which, int64_t rmax, cudaStream_t st);
 void launch_cg_a(const SolveConst& c, int64_t rmax, cudaStream_t st);
 void launch_cg_b(const SolveConst& c, int64_t rmax, cudaStream_t st);
 void launch_spmm_plain(int s, const int32_t* rp, const int32_t* ci, const double* val,

@@ -152,3 +152,57 @@ def test_golden_history_fixture(sk, po):
     f = np.array(g["config1_cg_reference_order"]["rel_residual"])
     assert h.size == f.size
     assert max_rel(h, f) <= 1e-10
+
+
+# ---------------------------------------------------------------- BiCGSTAB
+def test_bicgstab_identity_pair(sk, po):
+    """test_factorized_solvers.cpp:117-128: one iteration, X = C1 C2^T / 2 (exhaustion path)."""
+    i6, i4 = po.Csr.identity(6), po.Csr.identity(4)
+    c1, c2 = po.random_dense(6, 2, 30), po.random_dense(4, 2, 31)
+    ref = po.factorized_bicgstab(i6, i4, c1, c2, None, po.REPRODUCIBLE)
+    sol = sk.factorized_bicgstab(to_sk(sk, i6), to_sk(sk, i4), c1, c2)
+    _compare(sol, ref)
+    assert sol.status == "converged" and sol.history.iterations() == 1
+
+
+@pytest.mark.parametrize("n,m,s,seed", [(9, 7, 1, 32), (24, 21, 3, 48), (40, 40, 2, 5)])
+def test_bicgstab_diag_dominant_bitwise(sk, po, n, m, s, seed):
+    a, b = po.random_diag_dominant(n, seed), po.random_diag_dominant(m, seed + 1)
+    c1, c2 = po.random_dense(n, s, seed + 2), po.random_dense(m, s, seed + 3)
+    ref = po.factorized_bicgstab(a, b, c1, c2, po.Config(eps_tol=1e-9), po.REPRODUCIBLE)
+    sol = sk.factorized_bicgstab(to_sk(sk, a), to_sk(sk, b), c1, c2, sk.SolverConfig(eps_tol=1e-9))
+    _compare(sol, ref)
+
+
+@pytest.mark.parametrize("s", [1, 3, 4])
+def test_bicgstab_convdiff_bitwise(sk, po, s):
+    """ex4-desk style operator (problems.cpp:120-137): 3D convection-diffusion, grid 8."""
+    a = po.convection_diffusion_3d(8, (10.0, 10.0, 10.0))
+    c1, c2 = po.random_rhs(512, s, 99), po.random_rhs(512, s, 100)
+    cfg = po.Config(eps_tol=1e-8, max_iter=40)
+    ref = po.factorized_bicgstab(a, a, c1, c2, cfg, po.REPRODUCIBLE)
+    sol = sk.factorized_bicgstab(to_sk(sk, a), to_sk(sk, a), c1, c2, sk.SolverConfig(eps_tol=1e-8, max_iter=40))
+    _compare(sol, ref)
+
+
+def test_bicgstab_config2_shape_first_iterations(sk, po):
+    """BASELINE config 2 operators (2D convection-diffusion 256^2, Pe 10, winds (1,1)/(1,-1)),
+    s = 4, first 6 iterations bitwise against the oracle."""
+    a = po.convection_diffusion_2d(256, (10.0, 10.0))
+    b = po.convection_diffusion_2d(256, (10.0, -10.0))
+    c1, c2 = po.random_rhs(65536, 4, 1234), po.random_rhs(65536, 4, 1235)
+    ref = po.factorized_bicgstab(a, b, c1, c2, po.Config(eps_tol=1e-8, max_iter=6), po.REPRODUCIBLE)
+    sol = sk.factorized_bicgstab(to_sk(sk, a), to_sk(sk, b), c1, c2, sk.SolverConfig(eps_tol=1e-8, max_iter=6))
+    h = sol.history.rel_residuals()
+    assert bits_equal(h, ref.rel_residual), max_rel(h, ref.rel_residual)
+    assert bits_equal(sol.core, ref.core)
+
+
+def test_bicgstab_rank_bookkeeping(sk, po):
+    """RankBookkeepingIsExact (test_factorized_solvers.cpp:146-162)."""
+    a = po.convection_diffusion_3d(4, (10.0, 10.0, 10.0))
+    sol = sk.factorized_bicgstab(to_sk(sk, a), to_sk(sk, a), po.random_dense(64, 2, 36), po.random_dense(64, 2, 37),
+                                 sk.SolverConfig(eps_tol=1e-30, max_iter=4, capture_iterates=True))
+    assert sol.status == "max_iter" and len(sol.captured_cores) == 4
+    for k, core in enumerate(sol.captured_cores):
+        assert core.shape == ((2 * k + 2) * 2, (2 * k + 2) * 2)
