@@ -516,21 +516,23 @@ struct Solver {
     c.ccounter = ccounter;
   }
 
-  // packed upper block Hessenberg: column block e has (e+2)s rows at s^2 e(e+3)/2
-  static int64_t hpacked_size(int64_t steps, int64_t s) { return s * s * (steps * (steps + 3) / 2); }
+  // Arnoldi H: dense column-major, (steps+2)s rows x (steps+2)s columns capacity
   void ensure_hcap(int64_t steps) {
     if (!arnoldi || steps <= hcap_steps) return;
     int64_t ncap = std::max<int64_t>(steps, 2 * hcap_steps);
     ncap = std::max<int64_t>(std::min<int64_t>(ncap, cap_blocks), steps);
+    const int64_t nld = (ncap + 2) * s, old_ld = (hcap_steps + 2) * s;
     for (int sd = 0; sd < nsides; ++sd) {
       SideBuf& b = side[sd];
-      double* nh = dalloc<double>(hpacked_size(ncap, s));
+      double* nh = dalloc<double>(nld * nld);
       if (b.hband) {
-        CK(cudaMemcpyAsync(nh, b.hband, sizeof(double) * hpacked_size(hcap_steps, s), cudaMemcpyDeviceToDevice, st));
+        CK(cudaMemcpy2DAsync(nh, nld * sizeof(double), b.hband, old_ld * sizeof(double), old_ld * sizeof(double),
+                             old_ld, cudaMemcpyDeviceToDevice, st));
         dfree(b.hband);
       }
       b.hband = nh;
       c.side[sd].hband = nh;
+      c.side[sd].hld = nld;
     }
     if (nsides == 1) c.side[1] = c.side[0];
     hcap_steps = ncap;

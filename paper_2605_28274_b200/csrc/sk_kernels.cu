@@ -22,6 +22,8 @@
 #include "sk_device.cuh"
 #include "sk_launch.h"
 
+#include <cstdlib>
+
 namespace sk {
 
 __device__ __forceinline__ uint64_t globaltimer() {
@@ -73,10 +75,10 @@ __device__ inline int64_t first_block(const SolveConst& c, int64_t k) {
 __device__ inline double* hb_ptr(const SideConst& sc, int64_t e, int d, int s) {
   return sc.hband + (e * 3 + d) * (int64_t)(s * s);
 }
-// packed upper block Hessenberg (Arnoldi): column block e has (e+2)s rows
-__device__ __forceinline__ int64_t hcol_off(int64_t e, int s) { return (int64_t)s * s * (e * (e + 3) / 2); }
+// Arnoldi H: dense column-major with leading dimension hld (zero-initialised,
+// so the structural zeros below the block Hessenberg band read as 0.0)
 __device__ inline double* hcol_ptr(const SideConst& sc, int64_t e, int cc, int s) {
-  return sc.hband + hcol_off(e, s) + (int64_t)cc * (e + 2) * s;
+  return sc.hband + (e * s + cc) * sc.hld;
 }
 
 // coeff2 in the reference loop order (block_krylov.cpp:105-108)
@@ -347,6 +349,7 @@ __device__ __forceinline__ void raw_row_csr(const SideConst& sc, const double* _
 // are formed once per block; updates are x - sum_b U_b M_b.
 // =====================================================================
 constexpr int kFusedSegsPerCta = 8;
+enum UpdMode : int { UM_LANCZOS = 0, UM_FIRST = 1, UM_SECOND = 2, UM_CLEAN = 3, UM_INIT = 4 };
 
 template <int S>
 __device__ __forceinline__ void ld_raw(const double* __restrict__ x, int64_t i, double* u) {
@@ -985,9 +988,113 @@ __global__ void __launch_bounds__(256) k_gram_loop(SolveConst c) {
 }
 
 // =====================================================================
+// Arnoldi update (many blocks): one thread per (row, column) chain,
+// y(i,u) = x(i,u) - sum_b [sum_t U_b(i,t) M_b(t,u)] in ascending b (same
+// arithmetic as k_update); M and the block pointers staged in smem per chunk.
+// =====================================================================
+template <int S>
+__global__ void __launch_bounds__(256) k_arn_update(SolveConst c, int mode) {
+  constexpr int CH = 64;
+  const int side = blockIdx.y;
+  if (side >= c.nsides) return;
+  const DevState* st = c.st;
+  if (st->status != RUNNING) return;
+  const SideState& ss = st->side[side];
+  if (ss.exhausted || ss.broken) return;
+  const SideConst& sc = c.side[side];
+  const int64_t k = ss.blocks;
+  const double* xin = mode == UM_FIRST ? sc.w : sc.wx;
+  double* xout = mode == UM_FIRST ? sc.wx : sc.blocks[k];
+  const double* mc = mode == UM_FIRST ? sc.mcoef : sc.mcoef2;
+  const int64_t b0 = mode == UM_FIRST ? first_block(c, k) : 0, b1 = k;
+  const int64_t n = sc.n;
+  const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if ((int64_t)blockIdx.x * blockDim.x >= n * S) return;
+  const bool active = g < n * S;
+  const int64_t i = active ? g / S : n - 1;
+  const int u = (int)(g % S);
+  __shared__ double Ms[CH][S * S];
+  __shared__ const double* Bp[CH];
+  double y = __ldcg(xin + i * S + u);
+  for (int64_t cb = b0; cb < b1; cb += CH) {
+    const int nb = (int)mn64(CH, b1 - cb);
+    __syncthreads();
+    for (int e = threadIdx.x; e < nb * S * S; e += blockDim.x) Ms[e / (S * S)][e % (S * S)] = __ldcg(mc + (cb + e / (S * S)) * S * S + e % (S * S));
+    for (int e = threadIdx.x; e < nb; e += blockDim.x) Bp[e] = sc.blocks[cb + e];
+    __syncthreads();
+#pragma unroll 4
+    for (int b = 0; b < nb; ++b) {
+      double a[S];
+      ld_raw<S>(Bp[b], i, a);
+      double tmp = 0.0;
+#pragma unroll
+      for (int t = 0; t < S; ++t) tmp = __dadd_rn(tmp, __dmul_rn(a[t], Ms[b][u * S + t]));
+      y = __dsub_rn(y, tmp);
+    }
+  }
+  if (active) xout[i * S + u] = y;
+}
+
+// R1 self Gram x^T x of the candidate U_k (one warp per segment) + finalise.
+template <int S>
+__global__ void __launch_bounds__(256) k_self_gram(SolveConst c, int mode) {
+  constexpr int NS = S * (S + 1) / 2;
+  const int side = blockIdx.z;
+  if (side >= c.nsides) return;
+  const DevState* st = c.st;
+  if (st->status != RUNNING) return;
+  const SideState& ss = st->side[side];
+  if (ss.exhausted || ss.broken) return;
+  const SideConst& sc = c.side[side];
+  const int64_t nseg = sc.nseg;
+  const int64_t ncta = (nseg + kFusedSegsPerCta - 1) / kFusedSegsPerCta;
+  const int64_t cta = blockIdx.x;
+  if (cta >= ncta) return;
+  const double* __restrict__ x = sc.blocks[ss.blocks];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t seg = cta * kFusedSegsPerCta + warp;
+  const int nvalid_cta = (int)mn64(kFusedSegsPerCta, nseg - cta * kFusedSegsPerCta);
+  double acc[NS];
+#pragma unroll
+  for (int e = 0; e < NS; ++e) acc[e] = 0.0;
+  if (seg < nseg) {
+    const int64_t base = seg * kSeg;
+#pragma unroll 4
+    for (int m = 0; m < kLRows; ++m) {
+      const int64_t i = base + lane + 32 * m;
+      if (i < sc.n) {
+        double y[S];
+        ld_raw_cg<S>(x, i, y);
+        int e = 0;
+#pragma unroll
+        for (int u = 0; u < S; ++u)
+#pragma unroll
+          for (int t = 0; t <= u; ++t) {
+            acc[e] = __dadd_rn(acc[e], __dmul_rn(y[t], y[u]));
+            ++e;
+          }
+      }
+    }
+  }
+  warp_seg_to_cta<NS>(acc, nvalid_cta, sc.part + cta * NS);
+  if (!last_cta_arrive(sc.counter + 1, (unsigned)ncta)) return;
+  __shared__ double res[NS];
+  final_tree<NS>(sc.part, ncta, res);
+  SideState& sst = c.st->side[side];
+  for (int e = threadIdx.x; e < NS; e += blockDim.x) {
+    int t, u;
+    unpack_tri(e, t, u);
+    sst.gbase[u * S + t] = res[e];
+    sst.gbase[t * S + u] = res[e];
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) finalize_direct(c, side, true);
+  (void)mode;
+}
+
+// =====================================================================
 // x_out = x_in - sum_{b in [b0,b1)} U_b M_b (+ R1 Gram of x_out, finalise)
 // =====================================================================
-enum UpdMode : int { UM_LANCZOS = 0, UM_FIRST = 1, UM_SECOND = 2, UM_CLEAN = 3, UM_INIT = 4 };
 
 template <int S>
 __global__ void __launch_bounds__(256) k_update(SolveConst c, int mode) {
@@ -1633,6 +1740,8 @@ struct Launch {
   static void gram(const SolveConst& c, int mode, int64_t nblk, cudaStream_t st);
   static void update(const SolveConst& c, int mode, cudaStream_t st);
   static void householder(const SolveConst& c, int which, cudaStream_t st);
+  static void arn_update(const SolveConst& c, int mode, cudaStream_t st);
+  static void self_gram(const SolveConst& c, cudaStream_t st);
   static void lanczos_p1(const SolveConst& c, cudaStream_t st);
   static void lanczos_p2(const SolveConst& c, cudaStream_t st);
   static void gram_loop(const SolveConst& c, cudaStream_t st);
@@ -1670,6 +1779,15 @@ struct Launch {
   }
   static void householder(const SolveConst& c, int which, cudaStream_t st) {
     k_householder<S><<<c.nsides, 1024, 0, st>>>(c, which);
+  }
+  static void arn_update(const SolveConst& c, int mode, cudaStream_t st) {
+    int64_t nmax, cmax;
+    dims(c, nmax, cmax);
+    const unsigned g = (unsigned)((nmax * S + 255) / 256);
+    k_arn_update<S><<<dim3(g, c.nsides), 256, 0, st>>>(c, mode);
+  }
+  static void self_gram(const SolveConst& c, cudaStream_t st) {
+    k_self_gram<S><<<dim3(fused_grid(c), 1, c.nsides), 256, 0, st>>>(c, 0);
   }
   static unsigned fused_grid(const SolveConst& c) {
     int64_t m = 0;
@@ -1714,11 +1832,8 @@ template struct Launch<SK_INST_S>;
 // =====================================================================
 // BiCGSTAB (factorized_solvers.cpp:220-389) on the device
 // =====================================================================
-__device__ __forceinline__ double hpacked(const double* hb, int s, int64_t i, int64_t l) {
-  const int64_t e = l / s;
-  const int64_t hr = (e + 2) * s;
-  if (i >= hr) return 0.0;
-  return hb[hcol_off(e, s) + (l % s) * hr + i];
+__device__ __forceinline__ double hpacked(const double* hb, int64_t hld, int64_t i, int64_t l) {
+  return hb[l * hld + i];
 }
 
 // Dense core image with the upper block Hessenberg H (V side) and G (W side):
@@ -1739,6 +1854,7 @@ __global__ void __launch_bounds__(256) k_bi_image(SolveConst c, int which) {
   if (i0 >= ro || j0 >= co) return;
   const double* hv = c.side[0].hband;
   const double* hw = c.side[c.nsides > 1 ? 1 : 0].hband;
+  const int64_t hldv = c.side[0].hld, hldw = c.side[c.nsides > 1 ? 1 : 0].hld;
   __shared__ double As[kImK][kImT + 1], Bs[kImK][kImT + 1];
   const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
   double accH[4][4], accG[4][4];
@@ -1754,7 +1870,7 @@ __global__ void __launch_bounds__(256) k_bi_image(SolveConst c, int which) {
       for (int idx = threadIdx.x; idx < kImK * kImT; idx += blockDim.x) {
         const int kk = idx / kImT, ii = idx % kImT;
         const int64_t l = l0 + kk;
-        As[kk][ii] = (l < pr && i0 + ii < ro) ? hpacked(hv, s, i0 + ii, l) : 0.0;
+        As[kk][ii] = (l < pr && i0 + ii < ro) ? hpacked(hv, hldv, i0 + ii, l) : 0.0;
         Bs[kk][ii] = (l < pr && j0 + ii < pc) ? src[(j0 + ii) * ld + l] : 0.0;
       }
       __syncthreads();
@@ -1781,7 +1897,7 @@ __global__ void __launch_bounds__(256) k_bi_image(SolveConst c, int which) {
         const int kk = idx / kImT, ii = idx % kImT;
         const int64_t l = l0 + kk;
         As[kk][ii] = (l < pc && i0 + ii < pr) ? src[l * ld + i0 + ii] : 0.0;
-        Bs[kk][ii] = (l < pc && j0 + ii < co) ? hpacked(hw, s, j0 + ii, l) : 0.0;
+        Bs[kk][ii] = (l < pc && j0 + ii < co) ? hpacked(hw, hldw, j0 + ii, l) : 0.0;
       }
       __syncthreads();
 #pragma unroll
@@ -1808,6 +1924,117 @@ __global__ void __launch_bounds__(256) k_bi_image(SolveConst c, int which) {
       const bool hj = j < pc, gi = i < pr;
       const double q = (hj && gi) ? __dadd_rn(accH[a][b], accG[a][b]) : (hj ? accH[a][b] : (gi ? accG[a][b] : 0.0));
       dst[j * ld + i] = q;
+    }
+}
+
+// Register-blocked version: 128x128 output tile, 8x8 outputs per thread,
+// BK = 8 chunks double-buffered through registers -> smem. part 0 writes the
+// H part (columns j < pc); part 1 adds the G part per the presence rule. The
+// fma chain of every output runs over l in ascending order (bitwise the above).
+constexpr int kBM = 128, kBK = 8;
+__global__ void __launch_bounds__(256, 1) k_bi_image2(SolveConst c, int which, int part) {
+  DevState* st = c.st;
+  if (st->status != RUNNING) return;
+  const int s = c.s;
+  const double* src = which == 0 ? c.P[0] : c.S;
+  double* dst = which == 0 ? c.Q : c.T;
+  const int64_t pr = which == 0 ? st->rows_p : st->rows_s, pc = which == 0 ? st->cols_p : st->cols_s;
+  const int64_t ro = which == 0 ? st->rows_q : st->rows_t, co = which == 0 ? st->cols_q : st->cols_t;
+  const int64_t i0 = (int64_t)blockIdx.x * kBM, j0 = (int64_t)blockIdx.y * kBM;
+  if (i0 >= ro || j0 >= co) return;
+  const int64_t ld = c.ld;
+  const double* hv = c.side[0].hband;
+  const double* hw = c.side[c.nsides > 1 ? 1 : 0].hband;
+  const int64_t hldv = c.side[0].hld, hldw = c.side[c.nsides > 1 ? 1 : 0].hld;
+  // contraction range and operand roles
+  int64_t l_begin, l_end;
+  bool active;
+  if (part == 0) {
+    active = j0 < pc;
+    l_begin = (int64_t)s * mx64(0, i0 / s - 1);
+    l_end = pr;
+  } else {
+    active = i0 < pr;
+    l_begin = (int64_t)s * mx64(0, j0 / s - 1);
+    l_end = pc;
+  }
+  const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
+  __shared__ double As[2][kBK][kBM + 2], Bs[2][kBK][kBM + 2];
+  double acc[8][8];
+#pragma unroll
+  for (int a = 0; a < 8; ++a)
+#pragma unroll
+    for (int b = 0; b < 8; ++b) acc[a][b] = 0.0;
+  // each thread stages 4 A and 4 B values per chunk (8 x 128 = 1024 each)
+  double ra[4], rb[4];
+  auto fetch = [&](int64_t l0) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int idx = threadIdx.x + 256 * q;
+      const int kk = idx / kBM, mm = idx % kBM;
+      const int64_t l = l0 + kk;
+      const bool lin = l < l_end;
+      if (part == 0) {
+        const int64_t i = i0 + mm, j = j0 + mm;
+        ra[q] = (lin && i < ro) ? hpacked(hv, hldv, i, l) : 0.0;
+        rb[q] = (lin && j < pc) ? src[j * ld + l] : 0.0;
+      } else {
+        const int64_t i = i0 + mm, j = j0 + mm;
+        ra[q] = (lin && i < pr) ? src[l * ld + i] : 0.0;
+        rb[q] = (lin && j < co) ? hpacked(hw, hldw, j, l) : 0.0;
+      }
+    }
+  };
+  auto stash = [&](int buf) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int idx = threadIdx.x + 256 * q;
+      As[buf][idx / kBM][idx % kBM] = ra[q];
+      Bs[buf][idx / kBM][idx % kBM] = rb[q];
+    }
+  };
+  if (active && l_begin < l_end) {
+    fetch(l_begin);
+    stash(0);
+    __syncthreads();
+    int buf = 0;
+    for (int64_t l0 = l_begin; l0 < l_end; l0 += kBK) {
+      const bool more = l0 + kBK < l_end;
+      if (more) fetch(l0 + kBK);
+#pragma unroll
+      for (int kk = 0; kk < kBK; ++kk) {
+        double av[8], bv[8];
+#pragma unroll
+        for (int a = 0; a < 8; ++a) av[a] = As[buf][kk][ty + 16 * a];
+#pragma unroll
+        for (int b = 0; b < 8; ++b) bv[b] = Bs[buf][kk][tx + 16 * b];
+#pragma unroll
+        for (int a = 0; a < 8; ++a)
+#pragma unroll
+          for (int b = 0; b < 8; ++b) acc[a][b] = __fma_rn(av[a], bv[b], acc[a][b]);
+      }
+      if (more) {
+        stash(buf ^ 1);
+        __syncthreads();
+        buf ^= 1;
+      }
+    }
+  }
+#pragma unroll
+  for (int a = 0; a < 8; ++a)
+#pragma unroll
+    for (int b = 0; b < 8; ++b) {
+      const int64_t i = i0 + ty + 16 * a, j = j0 + tx + 16 * b;
+      if (i >= ro || j >= co) continue;
+      const bool hj = j < pc, gi = i < pr;
+      const int64_t o = j * ld + i;
+      if (part == 0) {
+        if (hj) dst[o] = acc[a][b];
+      } else {
+        if (hj && gi) dst[o] = __dadd_rn(dst[o], acc[a][b]);
+        else if (gi) dst[o] = acc[a][b];
+        else if (!hj) dst[o] = 0.0;
+      }
     }
 }
 
@@ -2101,16 +2328,23 @@ void launch_rare(const SolveConst& c, int64_t kmax_blocks, cudaStream_t st) {
 void launch_arnoldi_ext(const SolveConst& c, int64_t kmax_blocks, cudaStream_t st) {
   SK_DISPATCH_S(c.s, spmm(c, st));
   SK_DISPATCH_S(c.s, gram(c, (int)GM_ALL_W, kmax_blocks, st));
-  SK_DISPATCH_S(c.s, update(c, (int)UM_FIRST, st));
+  SK_DISPATCH_S(c.s, arn_update(c, (int)UM_FIRST, st));
   SK_DISPATCH_S(c.s, gram(c, (int)GM_ALL_X, kmax_blocks, st));
-  SK_DISPATCH_S(c.s, update(c, (int)UM_SECOND, st));
+  SK_DISPATCH_S(c.s, arn_update(c, (int)UM_SECOND, st));
+  SK_DISPATCH_S(c.s, self_gram(c, st));
   SK_DISPATCH_S(c.s, householder(c, 0, st));
-  g_launches += 6;
+  g_launches += 7;
 }
 void launch_bicgstab_half(const SolveConst& c, int which, int64_t rmax, cudaStream_t st) {
   k_bi_begin<<<1, 32, 0, st>>>(c, which);
-  const unsigned nt = (unsigned)((rmax + kImT - 1) / kImT);
-  k_bi_image<<<dim3(nt, nt), 256, 0, st>>>(c, which);
+  if (getenv("SK_SIMPLE_IMAGE")) {
+    const unsigned nt = (unsigned)((rmax + kImT - 1) / kImT);
+    k_bi_image<<<dim3(nt, nt), 256, 0, st>>>(c, which);
+  } else {
+    const unsigned nt = (unsigned)((rmax + kBM - 1) / kBM);
+    k_bi_image2<<<dim3(nt, nt), 256, 0, st>>>(c, which, 0);
+    k_bi_image2<<<dim3(nt, nt), 256, 0, st>>>(c, which, 1);
+  }
   if (which == 0) {
     k_bi_alpha<<<1, 32, 0, st>>>(c);
     k_bi_s<<<rows_grid(rmax * rmax), 256, 0, st>>>(c);
