@@ -1082,14 +1082,30 @@ int sko_basis_try_extend(sko_basis* b) {
     (void)hh;
     b->paths[b->mode == SKO_REPRODUCIBLE ? path : PATH_HOUSEHOLDER]++;
 
-    /* scale (:105-111) */
+    /* scale (:105-111). Reproducible Arnoldi: per-block sums in the reference's
+     * inner order, combined by the canonical pairwise tree over blocks. */
     double coeff2 = 0.0;
-    for (int64_t jb = first; jb < k; ++jb)
-        for (int64_t c = 0; c < s; ++c)
-            for (int64_t r = 0; r < s; ++r) {
-                const double h = hcoef[jb * ss + c * s + r];
-                coeff2 = coeff2 + h * h;
-            }
+    if (b->mode == SKO_REPRODUCIBLE && b->arnoldi) {
+        double* hsq = (double*)xcalloc((size_t)(k - first + 1), sizeof(double));
+        for (int64_t jb = first; jb < k; ++jb) {
+            double acc = 0.0;
+            for (int64_t c = 0; c < s; ++c)
+                for (int64_t r = 0; r < s; ++r) {
+                    const double h = hcoef[jb * ss + c * s + r];
+                    acc = acc + h * h;
+                }
+            hsq[jb - first] = acc;
+        }
+        coeff2 = tree_reduce(hsq, k - first);
+        free(hsq);
+    } else {
+        for (int64_t jb = first; jb < k; ++jb)
+            for (int64_t c = 0; c < s; ++c)
+                for (int64_t r = 0; r < s; ++r) {
+                    const double h = hcoef[jb * ss + c * s + r];
+                    coeff2 = coeff2 + h * h;
+                }
+    }
     double r2 = 0.0;
     for (int64_t e = 0; e < ss; ++e) r2 = r2 + R[e] * R[e];
     const double scale = sqrt(b->hfro2 + coeff2 + r2);

@@ -86,6 +86,7 @@ struct SideConst {
   double* coef2;             // [cap_blocks][s*s] second-pass coefficients
   double* mcoef;             // [cap_blocks][s*s] M_b = N_b^{-1} c_b (pass 1)
   double* mcoef2;            // [cap_blocks][s*s] second-pass M_b
+  double* hsq;               // [cap_blocks] Arnoldi: per-block sum of squared H coefficients
   double* part;              // R1 CTA partials
   unsigned int* counter;     // last-CTA counters (several slots)
   int64_t ncta;              // CTAs covering n rows (kRowsPerCta each)

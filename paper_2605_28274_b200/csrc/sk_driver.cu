@@ -283,7 +283,7 @@ struct SideBuf {
   int64_t n = 0;
   double *w = nullptr, *wx = nullptr, *qh = nullptr, *hw = nullptr;
   double *hband = nullptr, *coef = nullptr, *coef2 = nullptr, *part = nullptr, *nfac = nullptr;
-  double *mcoef = nullptr, *mcoef2 = nullptr;
+  double *mcoef = nullptr, *mcoef2 = nullptr, *hsq = nullptr;
   unsigned int* counter = nullptr;
   double** table = nullptr;
   double** table_host = nullptr;  // pinned mirror (async uploads)
@@ -422,6 +422,7 @@ struct Solver {
       b.coef2 = dalloc<double>(cap_blocks * s * s);
       b.mcoef = dalloc<double>(cap_blocks * s * s);
       b.mcoef2 = dalloc<double>(cap_blocks * s * s);
+      b.hsq = dalloc<double>(cap_blocks + 8);
       b.part = dalloc<double>(std::max<int64_t>((cap_blocks + 3) * ncta * s * s, 2 * nseg * s * s + 64));
       b.counter = dalloc<unsigned int>(cap_blocks + 8);
       b.table = dalloc<double*>(cap_blocks);
@@ -443,6 +444,7 @@ struct Solver {
       sc.coef2 = b.coef2;
       sc.mcoef = b.mcoef;
       sc.mcoef2 = b.mcoef2;
+      sc.hsq = b.hsq;
       sc.part = b.part;
       sc.counter = b.counter;
       sc.ncta = ncta;
@@ -773,6 +775,7 @@ struct Solver {
       dfree(b.coef2);
       dfree(b.mcoef);
       dfree(b.mcoef2);
+      dfree(b.hsq);
       dfree(b.part);
       dfree(b.counter);
       dfree(b.table);

@@ -81,21 +81,56 @@ __device__ inline double* hcol_ptr(const SideConst& sc, int64_t e, int cc, int s
   return sc.hband + (e * s + cc) * sc.hld;
 }
 
-// coeff2 in the reference loop order (block_krylov.cpp:105-108)
+// coeff2 (block_krylov.cpp:105-108): Lanczos in the reference loop order; Arnoldi
+// as the canonical tree over per-block sums hsq[b] (written by the Gram pass).
 __device__ inline double coeff2_of(const SolveConst& c, int side, int64_t k, int64_t e) {
   const SideConst& sc = c.side[side];
   const int s = c.s, ss = s * s;
+  if (c.arnoldi) {
+    TreeStream ts;
+    ts.init();
+    for (int64_t jb = 0; jb < k; ++jb) ts.push(__ldcg(sc.hsq + jb));
+    return ts.finish();
+  }
   double acc = 0.0;
   for (int64_t jb = first_block(c, k); jb < k; ++jb)
     for (int cc = 0; cc < s; ++cc)
       for (int r = 0; r < s; ++r) {
-        const double h = c.arnoldi ? __ldcg(hcol_ptr(sc, e, cc, s) + jb * s + r)
-                                   : __ldcg(sc.coef + jb * ss + cc * s + r);
+        const double h = __ldcg(sc.coef + jb * ss + cc * s + r);
         acc = __dadd_rn(acc, __dmul_rn(h, h));
       }
+  (void)e;
   return acc;
 }
-
+// block-parallel canonical tree over a[0..count) (all threads; result to all)
+static __device__ double block_tree(const double* a, int64_t count, double* sbuf /* >= 1024 */) {
+  // level 1: aligned groups of 8 per thread, then a stream over the group nodes
+  __shared__ double res;
+  const int64_t ng = (count + 7) / 8;
+  for (int64_t g = threadIdx.x; g < ng; g += blockDim.x) {
+    double v[8];
+    const int cnt = (int)mn64(8, count - 8 * g);
+    for (int j = 0; j < cnt; ++j) v[j] = __ldcg(a + 8 * g + j);
+    double node = tree_reduce_local(v, cnt);
+    if (ng <= 1024) sbuf[g] = node;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    if (ng <= 1024) {
+      TreeStream ts;
+      ts.init();
+      for (int64_t g = 0; g < ng; ++g) ts.push(sbuf[g]);
+      res = ts.finish();
+    } else {
+      TreeStream ts;
+      ts.init();
+      for (int64_t j = 0; j < count; ++j) ts.push(__ldcg(a + j));
+      res = ts.finish();
+    }
+  }
+  __syncthreads();
+  return res;
+}
 __device__ inline void set_nfac(const SideConst& sc, int64_t b, int s, const double* N, bool identity) {
   double* p = sc.nfac + b * (s * s + s);
   for (int e = 0; e < s * s; ++e) p[e] = identity ? ((e % (s + 1)) == 0 ? 1.0 : 0.0) : N[e];
@@ -173,7 +208,8 @@ __device__ inline void classify(const SolveConst& c, int side, bool first_pass, 
   SideState& st = c.st->side[side];
   const int s = c.s, ss = s * s;
   if (first_pass) {
-    st.coeff2 = coeff2_of(c, side, st.blocks, st.steps);
+    if (!(c.arnoldi && st.pad == 1)) st.coeff2 = coeff2_of(c, side, st.blocks, st.steps);
+    st.pad = 0;
     double r2 = 0.0;
     for (int x = 0; x < ss; ++x) r2 = __dadd_rn(r2, __dmul_rn(st.R[x], st.R[x]));
     st.r2 = r2;
@@ -698,11 +734,16 @@ __global__ void __launch_bounds__(256) k_gram(SolveConst c, int mode) {
       mout[b * NB + e] = mb[e];
     }
     if (mode == GM_ALL_X && c.arnoldi) {
-      // H column = first + second CGS pass (block_krylov.cpp:87-93)
+      // H column = first + second CGS pass (block_krylov.cpp:87-93); hsq[b] =
+      // its sum of squares in the reference's (column, row) order
+      double hsq = 0.0;
       for (int e = 0; e < NB; ++e) {
         const int t = e % S, u = e / S;
-        hcol_ptr(sc, c.st->side[side].steps, u, S)[b * S + t] = __dadd_rn(__ldcg(sc.coef + b * NB + e), cb[e]);
+        const double h = __dadd_rn(__ldcg(sc.coef + b * NB + e), cb[e]);
+        hcol_ptr(sc, c.st->side[side].steps, u, S)[b * S + t] = h;
+        hsq = __dadd_rn(hsq, __dmul_rn(h, h));
       }
+      sc.hsq[b] = hsq;
     }
   }
 }
@@ -1088,6 +1129,14 @@ __global__ void __launch_bounds__(256) k_self_gram(SolveConst c, int mode) {
     sst.gbase[t * S + u] = res[e];
   }
   __syncthreads();
+  if (c.arnoldi) {
+    __shared__ double sbuf[1024];
+    const double c2 = block_tree(sc.hsq, sst.blocks, sbuf);
+    if (threadIdx.x == 0) {
+      sst.coeff2 = c2;
+      sst.pad = 1;  // coeff2 precomputed for this step
+    }
+  }
   if (threadIdx.x == 0) finalize_direct(c, side, true);
   (void)mode;
 }
@@ -1959,13 +2008,18 @@ __global__ void __launch_bounds__(256, 1) k_bi_image2(SolveConst c, int which, i
     l_end = pc;
   }
   const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
-  __shared__ double As[2][kBK][kBM + 2], Bs[2][kBK][kBM + 2];
+  // row stride 132 doubles: the transposed (kk-fastest) stores below hit each
+  // bank pair at most twice per warp (the 2-wavefront minimum for 256 B)
+  __shared__ double As[2][kBK][kBM + 4], Bs[2][kBK][kBM + 4];
   double acc[8][8];
 #pragma unroll
   for (int a = 0; a < 8; ++a)
 #pragma unroll
     for (int b = 0; b < 8; ++b) acc[a][b] = 0.0;
-  // each thread stages 4 A and 4 B values per chunk (8 x 128 = 1024 each)
+  // each thread stages 4 A and 4 B values per chunk (8 x 128 = 1024 each).
+  // Operands contiguous along m use idx -> (kk = idx / 128, m = idx % 128); the
+  // part-0 B operand (the core, contiguous along l) uses kk = idx % 8, m = idx / 8
+  // so a warp reads 4 columns x 64 contiguous bytes.
   double ra[4], rb[4];
   auto fetch = [&](int64_t l0) {
 #pragma unroll
@@ -1975,9 +2029,11 @@ __global__ void __launch_bounds__(256, 1) k_bi_image2(SolveConst c, int which, i
       const int64_t l = l0 + kk;
       const bool lin = l < l_end;
       if (part == 0) {
-        const int64_t i = i0 + mm, j = j0 + mm;
+        const int kt = idx % kBK, mt = idx / kBK;
+        const int64_t lt = l0 + kt;
+        const int64_t i = i0 + mm, j = j0 + mt;
         ra[q] = (lin && i < ro) ? hpacked(hv, hldv, i, l) : 0.0;
-        rb[q] = (lin && j < pc) ? src[j * ld + l] : 0.0;
+        rb[q] = (lt < l_end && j < pc) ? src[j * ld + lt] : 0.0;
       } else {
         const int64_t i = i0 + mm, j = j0 + mm;
         ra[q] = (lin && i < pr) ? src[l * ld + i] : 0.0;
@@ -1990,7 +2046,10 @@ __global__ void __launch_bounds__(256, 1) k_bi_image2(SolveConst c, int which, i
     for (int q = 0; q < 4; ++q) {
       const int idx = threadIdx.x + 256 * q;
       As[buf][idx / kBM][idx % kBM] = ra[q];
-      Bs[buf][idx / kBM][idx % kBM] = rb[q];
+      if (part == 0)
+        Bs[buf][idx % kBK][idx / kBK] = rb[q];
+      else
+        Bs[buf][idx / kBM][idx % kBM] = rb[q];
     }
   };
   if (active && l_begin < l_end) {
