@@ -126,6 +126,43 @@ sk_status sk_solution_captured_core(const sk_solution* sol, int64_t i, int64_t* 
 sk_status sk_solution_stats(const sk_solution* sol, sk_solve_stats* out);
 void sk_solution_free(sk_solution* sol);
 
+/* Row partition (the reference has no multi-GPU path -- this is
+ * the north star's "A's rows and B's rows partitioned across GPUs"). Rows are
+ * split on reduction chunks (aligned power-of-two groups of 512-row R1
+ * segments), so every rank's history, cores and classification decisions are
+ * bitwise those of the single-GPU solve. Per iteration: one all-gather of the
+ * Gram chunk nodes per pass and one halo exchange of the newest basis block.
+ * CG and Lyapunov CG with s <= 4. */
+typedef struct sk_comm sk_comm;
+typedef struct sk_partition {
+  int64_t row0, rows;          /* this rank's global rows [row0, row0 + rows) */
+  int64_t chunk_rows;          /* rows per reduction chunk */
+  int64_t chunks, chunks_max, chunks_total;
+  int64_t halo;                /* ghost rows per side (one grid line / plane, or the bandwidth) */
+} sk_partition;
+/* Pure host function: the plan every rank computes identically. */
+sk_status sk_partition_plan(int64_t n, int64_t halo, int32_t world, int32_t rank, sk_partition* out);
+/* NCCL transport (one process per GPU): rank 0 makes the id, the caller
+ * broadcasts it (e.g. torch.distributed), every rank creates its communicator.
+ * libnccl.so.2 is loaded at run time. */
+sk_status sk_nccl_unique_id(uint8_t* out128);
+sk_status sk_comm_create_nccl(const uint8_t* id128, int32_t nranks, int32_t rank, int32_t device,
+                              sk_comm** out);
+/* In-process group: nranks communicators whose ranks are host threads (one
+ * solve per thread); collectives are device copies behind host barriers. */
+sk_status sk_comm_create_local_group(int32_t nranks, sk_comm** out /* nranks entries */);
+int32_t sk_comm_rank(const sk_comm* c);
+int32_t sk_comm_size(const sk_comm* c);
+void sk_comm_free(sk_comm* c);
+/* Every rank passes the whole A, B, C1, C2 (host) and keeps only its rows. */
+sk_status sk_problem_create_partitioned(int32_t method, const sk_csr* a, const sk_csr* b,
+                                        const double* c1, const double* c2, int64_t s,
+                                        const sk_gpu_options* gpu, sk_comm* comm, sk_problem** out);
+/* Partitioned solutions hold this rank's rows of V and W (sk_solution_dims
+ * then reports the local row counts). */
+sk_status sk_solution_partition(const sk_solution* sol, int64_t* row0_v, int64_t* rows_v,
+                                int64_t* row0_w, int64_t* rows_w);
+
 const char* sk_last_error(void);
 const char* sk_version(void);
 int32_t sk_device_count(void);

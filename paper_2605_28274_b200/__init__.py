@@ -250,6 +250,10 @@ class FactorizedSolution:
             buf = np.zeros((r_.value, c_.value), order="F")
             _check(L.sk_solution_captured_core(handle, C.c_int64(i), C.byref(r_), C.byref(c_), _p(buf)))
             self.captured_cores.append(buf)
+        # row partition: this rank's global row offsets of V and W (0 on one GPU)
+        r0v, r0w = C.c_int64(), C.c_int64()
+        _check(L.sk_solution_partition(handle, C.byref(r0v), None, C.byref(r0w), None))
+        self.row0_v, self.row0_w = r0v.value, r0w.value
         self._V = self._W = self._core = None
 
     @property
@@ -389,3 +393,113 @@ def spmm(a: SparseMatrix, x, transpose: bool = False) -> np.ndarray:
     ca = a._c()
     _check(lib().sk_spmm(C.byref(ca), _p(x), C.c_int64(x.shape[1]), C.c_int32(int(transpose)), _p(y)))
     return y
+
+
+# ---------------------------------------------------------------------------
+# Row partition: multi-GPU CG / Lyapunov CG
+# ---------------------------------------------------------------------------
+class _Partition(C.Structure):
+    _fields_ = [(f, C.c_int64) for f in
+                ("row0", "rows", "chunk_rows", "chunks", "chunks_max", "chunks_total", "halo")]
+
+
+def partition_plan(n: int, halo: int, world: int, rank: int) -> dict:
+    """The row split every rank computes identically (sk_partition_plan; host only)."""
+    out = _Partition()
+    _check(lib().sk_partition_plan(C.c_int64(n), C.c_int64(halo), C.c_int32(world), C.c_int32(rank),
+                                   C.byref(out)))
+    return {f: getattr(out, f) for f, _ in _Partition._fields_}
+
+
+class Communicator:
+    """Collectives of the row-partitioned solve: NCCL (one process per GPU) or an
+    in-process group whose ranks are host threads (sk_comm)."""
+
+    def __init__(self, handle):
+        self._h = handle
+        self.rank = int(lib().sk_comm_rank(handle))
+        self.size = int(lib().sk_comm_size(handle))
+
+    @staticmethod
+    def nccl_unique_id() -> bytes:
+        buf = (C.c_uint8 * 128)()
+        _check(lib().sk_nccl_unique_id(buf))
+        return bytes(buf)
+
+    @classmethod
+    def nccl(cls, uid: bytes, nranks: int, rank: int, device: int) -> "Communicator":
+        if len(uid) != 128:
+            raise DimensionError("NCCL unique id must be 128 bytes")
+        buf = (C.c_uint8 * 128).from_buffer_copy(uid)
+        h = C.c_void_p()
+        _check(lib().sk_comm_create_nccl(buf, C.c_int32(nranks), C.c_int32(rank), C.c_int32(device),
+                                         C.byref(h)))
+        return cls(h)
+
+    @classmethod
+    def local_group(cls, nranks: int) -> list:
+        hs = (C.c_void_p * nranks)()
+        _check(lib().sk_comm_create_local_group(C.c_int32(nranks), hs))
+        return [cls(C.c_void_p(h)) for h in hs]
+
+    def free(self):
+        if getattr(self, "_h", None):
+            lib().sk_comm_free(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+
+class PartitionedProblem(ResidentProblem):
+    """This rank's rows of a CG / Lyapunov CG problem (sk_problem_create_partitioned).
+    Every rank passes the whole operators and right-hand sides; solve() must be
+    called by all ranks of the communicator together."""
+
+    def __init__(self, method: str, a: SparseMatrix, b: Optional[SparseMatrix], c1, c2,
+                 comm: Communicator, gpu: Optional[GpuOptions] = None):
+        c1 = _mat(c1, a.n_rows, "C1")
+        c2a = _mat(c2, b.n_rows, "C2") if c2 is not None else None
+        self._keep = [c1, c2a, comm]
+        ca = a._c()
+        cb = b._c() if b is not None else None
+        gpu_c = (gpu or GpuOptions())._c()
+        h = C.c_void_p()
+        _check(lib().sk_problem_create_partitioned(
+            C.c_int32(METHODS[method]), C.byref(ca), C.byref(cb) if cb is not None else None, _p(c1),
+            _p(c2a) if c2a is not None else None, C.c_int64(c1.shape[1]), C.byref(gpu_c), comm._h,
+            C.byref(h)))
+        self._h = h
+
+
+def solve_local_group(method: str, a: SparseMatrix, b: Optional[SparseMatrix], c1, c2, world: int,
+                      cfg: Optional[SolverConfig] = None, gpu: Optional[GpuOptions] = None) -> list:
+    """Runs the row-partitioned solve with `world` ranks as host threads of this
+    process (sk_comm_create_local_group); returns every rank's solution."""
+    import threading
+
+    comms = Communicator.local_group(world)
+    sols, errs = [None] * world, [None] * world
+    probs = [None] * world
+
+    def run(r):
+        try:
+            probs[r] = PartitionedProblem(method, a, b, c1, c2, comms[r], gpu)
+            sols[r] = probs[r].solve(cfg)
+        except BaseException as e:  # surfaced after join
+            errs[r] = e
+
+    ts = [threading.Thread(target=run, args=(r,)) for r in range(world)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    for e in errs:
+        if e is not None:
+            raise e
+    for p in probs:
+        p.free()
+    return sols

@@ -27,6 +27,7 @@ def units():
     u.append(("sk_kernels.cu", "sk_kernels_common.o", ["-DSK_INST_COMMON"]))
     u.append(("sk_driver.cu", "sk_driver.o", []))
     u.append(("sk_problems.cpp", "sk_problems.o", []))
+    u.append(("sk_comm.cpp", "sk_comm.o", []))
     return u
 
 
@@ -43,7 +44,8 @@ def needs_build() -> bool:
 def _compile(unit, verbose):
     src, obj, defs = unit
     if src.endswith(".cpp"):
-        cmd = ["g++", "-O3", "-std=c++17", "-fPIC", "-Wall", "-ffp-contract=off", "-pthread", *defs,
+        cmd = ["g++", "-O3", "-std=c++17", "-fPIC", "-Wall", "-ffp-contract=off", "-pthread",
+               "-I/usr/local/cuda/include", *defs,
                "-c", os.path.join(CSRC, src), "-o", os.path.join(CSRC, obj)]
     else:
         cmd = [NVCC, *FLAGS, *defs, "-c", os.path.join(CSRC, src), "-o", os.path.join(CSRC, obj)]
@@ -66,7 +68,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
             sys.stderr.write(lg)
     objs = [os.path.join(CSRC, u[1]) for u in us]
     subprocess.check_call([NVCC, "-shared", *ARCH, *objs, "-o", LIB + ".tmp", "-lcudart",
-                           "-Xcompiler", "-pthread"])
+                           "-Xcompiler", "-pthread", "-ldl"])
     os.replace(LIB + ".tmp", LIB)
     return LIB
 

@@ -24,7 +24,8 @@ constexpr int kMaxS = 8;                   // device block-size limit
 constexpr double kPythGuard = 0x1p-10;
 constexpr double kHHRatio = 1e-6;
 
-enum Status : int { RUNNING = 0, CONVERGED = 1, MAXITER = 2, BREAKDOWN = 3, RANKDEF = 4, FAILED = 5 };
+enum Status : int { RUNNING = 0, CONVERGED = 1, MAXITER = 2, BREAKDOWN = 3, RANKDEF = 4, FAILED = 5,
+                    PAUSED = 6 /* row partition: a rare path waits for the host-driven sequence */ };
 
 // per-extension stage machine of one basis side
 enum Stage : int {
@@ -98,6 +99,17 @@ struct SideConst {
   int32_t sg_pow2;           // log2(g) if g is a power of two, else -1
   int64_t sg;                // grid edge g
   double scoef[7];           // values by ascending offset
+  // row partition (SolveConst::world > 1): local rows are global rows
+  // [row0, row0 + n); block storage carries `halo` ghost rows on each side.
+  int64_t row0;
+  int32_t dist;              // 1: last CTAs emit chunk nodes instead of finalising
+  int32_t pad_;
+  int64_t chunk_f;           // fused-kernel CTAs (8 segments) per reduction chunk
+  int64_t chunk_g;           // general-kernel CTAs (32 segments) per reduction chunk
+  int64_t nch;               // local reduction chunks
+  int64_t halo;              // ghost rows per side of a block (0: none)
+  double* hsend;             // [2][halo][s] first / last local rows of the newest block
+  double* hrecv;             // [2][halo][s] rows received from the previous / next rank
 };
 
 struct SolveConst {
@@ -116,6 +128,14 @@ struct SolveConst {
   double* T;      // BiCGSTAB image of S
   double* Rs;     // BiCGSTAB shadow residual (s x s)
   int64_t ld;
+  // row partition: reduction-chunk nodes (outbound, this rank) and the
+  // all-gathered messages of every rank (inbound), see sk_kernels.cu "partition"
+  int32_t world, rank;
+  int64_t nch_max;         // chunk slots per (slot, side) in a message
+  int64_t nex;             // doubles per node (2 s^2)
+  const int32_t* rank_nch; // [world] chunks owned by each rank
+  double* nodes;
+  double* gnodes;
   double* cpart;  // R2 tile partials
   unsigned int* ccounter;
   double* hist_rel;   // [max_iter+1]

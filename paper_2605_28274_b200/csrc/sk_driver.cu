@@ -8,6 +8,7 @@
 #include "../../include/sylkrylov_b200.h"
 #include "sk_device.cuh"
 #include "sk_launch.h"
+#include "sk_comm.h"
 
 #include <algorithm>
 #include <cstdio>
@@ -204,7 +205,7 @@ struct DevCsr {
 };
 
 size_t upload_csr(DevCsr& d, int64_t n, int64_t nnz, const int64_t* rp, const int64_t* ci,
-                  const double* val, cudaStream_t st) {
+                  const double* val, cudaStream_t st, bool detect = true) {
   if (n >= (int64_t(1) << 31) || nnz >= (int64_t(1) << 31))
     throw SkError(SK_ERR_UNSUPPORTED, "device CSR uses int32 indices: n and nnz must be < 2^31");
   std::vector<int32_t> rp32(n + 1), ci32(std::max<int64_t>(nnz, 1));
@@ -212,7 +213,7 @@ size_t upload_csr(DevCsr& d, int64_t n, int64_t nnz, const int64_t* rp, const in
   for (int64_t k = 0; k < nnz; ++k) ci32[k] = (int32_t)ci[k];
   d.n = n;
   d.nnz = nnz;
-  if (!getenv("SK_NO_STENCIL")) detect_stencil(rp, ci, val, n, d.stencil);
+  if (detect && !getenv("SK_NO_STENCIL")) detect_stencil(rp, ci, val, n, d.stencil);
   CK(cudaMalloc(&d.rp, sizeof(int32_t) * (n + 1)));
   CK(cudaMalloc(&d.ci, sizeof(int32_t) * std::max<int64_t>(nnz, 1)));
   CK(cudaMalloc(&d.val, sizeof(double) * std::max<int64_t>(nnz, 1)));
@@ -222,6 +223,51 @@ size_t upload_csr(DevCsr& d, int64_t n, int64_t nnz, const int64_t* rp, const in
   CK(cudaStreamSynchronize(st));  // host staging vectors go out of scope
   return sizeof(int32_t) * (n + 1 + nnz) + sizeof(double) * nnz;
 }
+// ---------------------------------------------------------------------------
+// Row partition plan. Rows are split on reduction chunks: aligned
+// groups of cs R1 segments, cs a power of two >= 32 (one general-kernel CTA),
+// chosen as large as keeps >= 4 chunks per rank. Rank r owns chunks
+// [r T / G, (r+1) T / G). Every rank needs >= halo rows so ghost rows come only
+// from the two neighbours.
+// ---------------------------------------------------------------------------
+struct Plan {
+  int64_t n = 0, halo = 0, chunk_rows = 0, total = 0, nch_max = 0;
+  std::vector<int64_t> row0, rows, nch;
+};
+Plan make_plan(int64_t n, int64_t halo, int world) {
+  if (world < 1) throw SkError(SK_ERR_DIMENSION, "row partition: world size must be >= 1");
+  Plan p;
+  p.n = n;
+  p.halo = world > 1 ? halo : 0;
+  const int64_t nseg = (n + sk::kSeg - 1) / sk::kSeg;
+  int64_t cs = sk::kSegsPerCta;
+  if ((nseg + cs - 1) / cs < world)
+    throw SkError(SK_ERR_UNSUPPORTED, "row partition: too few rows for the world size (needs >= " +
+                                          std::to_string(cs * sk::kSeg) + " rows per rank)");
+  while ((nseg + 2 * cs - 1) / (2 * cs) >= 4 * (int64_t)world) cs *= 2;
+  p.chunk_rows = cs * sk::kSeg;
+  p.total = (nseg + cs - 1) / cs;
+  for (int r = 0; r < world; ++r) {
+    const int64_t c0 = r * p.total / world, c1 = (r + 1) * p.total / world;
+    p.row0.push_back(c0 * p.chunk_rows);
+    p.rows.push_back(std::min<int64_t>(n, c1 * p.chunk_rows) - c0 * p.chunk_rows);
+    p.nch.push_back(c1 - c0);
+    p.nch_max = std::max<int64_t>(p.nch_max, c1 - c0);
+    if (world > 1 && p.rows.back() < halo)
+      throw SkError(SK_ERR_UNSUPPORTED, "row partition: a rank holds fewer rows than the operator halo");
+  }
+  return p;
+}
+// ghost rows a row block needs: one grid line (2D) / plane (3D), else the bandwidth
+int64_t operator_halo(const int64_t* rp, const int64_t* ci, int64_t n, const StencilInfo& si) {
+  if (si.dim == 2) return si.g;
+  if (si.dim == 3) return si.g * si.g;
+  int64_t h = 0;
+  for (int64_t i = 0; i < n; ++i)
+    for (int64_t k = rp[i]; k < rp[i + 1]; ++k) h = std::max<int64_t>(h, std::llabs(ci[k] - i));
+  return h;
+}
+
 void free_csr(DevCsr& d) {
   cudaFree(d.rp);
   cudaFree(d.ci);
@@ -247,6 +293,15 @@ struct sk_problem {
   cudaStream_t stream = nullptr;
   int64_t h2d_bytes = 0;
   double h2d_time = 0.0;
+  // row partition (world > 1): this rank's rows of each side; c1/c2 stay whole
+  sk::Comm* comm = nullptr;  // caller-owned
+  int world = 1, rank = 0;
+  Plan plan[2];
+  int64_t nglob[2] = {0, 0};
+};
+
+struct sk_comm {
+  std::unique_ptr<sk::Comm> impl;
 };
 
 // ---------------------------------------------------------------------------
@@ -269,6 +324,7 @@ struct sk_solution {
   std::vector<double*> chunks;            // owned allocations
   double* X = nullptr;                    // owned core buffer
   int64_t ld = 0;
+  int64_t row0_v = 0, row0_w = 0;         // row partition: first global row of V / W here
 };
 
 namespace {
@@ -289,6 +345,14 @@ struct SideBuf {
   double** table_host = nullptr;  // pinned mirror (async uploads)
   std::vector<double*> blocks;
   int64_t cap_blocks = 0, hld = 0;
+  // row partition
+  int64_t halo = 0;
+  double *hsend = nullptr, *hrecv = nullptr;
+  // full view (whole column block on every rank) for init / Householder
+  int64_t nglob = 0;
+  double *F = nullptr, *fwx = nullptr, *fqh = nullptr, *fhw = nullptr, *fpart = nullptr;
+  unsigned int* fcounter = nullptr;
+  double** ftable = nullptr;
 };
 
 struct Solver {
@@ -309,6 +373,10 @@ struct Solver {
   double *hist_rel = nullptr, *hist_tk = nullptr, *hist_tb = nullptr;
   sk::DevState* dstate = nullptr;
   sk::SolveConst c{};
+  // row partition (P.world > 1)
+  bool dist = false;
+  int32_t* rank_nch = nullptr;
+  double *nodes = nullptr, *gnodes = nullptr;
   // profiling
   struct Ev {
     cudaEvent_t a, b;
@@ -402,10 +470,14 @@ struct Solver {
     c.tol = cfg.breakdown_tol;
     c.eps = cfg.eps_tol;
     c.max_iter = max_iter;
+    dist = P.world > 1;
+    if (dist && (arnoldi || !sk::lanczos_fused_ok(c)))
+      throw SkError(SK_ERR_UNSUPPORTED, "row partition: CG / Lyapunov CG with s <= 4 (no full reorthogonalisation)");
     for (int sd = 0; sd < nsides; ++sd) {
       SideBuf& b = side[sd];
       const DevCsr& op = P.op[sd];
       b.n = op.n;
+      b.halo = dist ? P.plan[sd].halo : 0;
       const int64_t ns = b.n * s;
       const int64_t ncta = (b.n + sk::kRowsPerCta - 1) / sk::kRowsPerCta;
       const int64_t nseg = (b.n + sk::kSeg - 1) / sk::kSeg;
@@ -458,8 +530,10 @@ struct Solver {
         sc.sg_pow2 = sh;
       }
       for (int q = 0; q < 7; ++q) sc.scoef[q] = op.stencil.c[q];
+      if (dist) setup_partition(sd);
     }
     if (nsides == 1) c.side[1] = c.side[0];
+    if (dist) setup_nodes();
     dstate = dalloc<sk::DevState>(1);
     hist_rel = dalloc<double>(max_iter + 2);
     hist_tk = dalloc<double>(max_iter + 2);
@@ -474,6 +548,168 @@ struct Solver {
       ensure_hcap(std::min<int64_t>(cap_blocks, 64));
     }
     grow_cores(std::min<int64_t>((arnoldi ? 2 * max_iter + 3 : max_iter + 2) * s, 512));
+  }
+
+  // ---- row partition ----
+  void setup_partition(int sd) {
+    SideBuf& b = side[sd];
+    const Plan& pl = P.plan[sd];
+    sk::SideConst& sc = c.side[sd];
+    sc.row0 = pl.row0[P.rank];
+    sc.dist = 1;
+    sc.chunk_f = pl.chunk_rows / (sk::kSeg * 8);  // kFusedSegsPerCta
+    sc.chunk_g = pl.chunk_rows / sk::kRowsPerCta;
+    sc.nch = pl.nch[P.rank];
+    sc.halo = b.halo;
+    b.hsend = dalloc<double>(2 * b.halo * s + 1);
+    b.hrecv = dalloc<double>(2 * b.halo * s + 1);
+    sc.hsend = b.hsend;
+    sc.hrecv = b.hrecv;
+    // full view
+    b.nglob = P.nglob[sd];
+    const int64_t ng = b.nglob * s;
+    const int64_t nseg_g = (b.nglob + sk::kSeg - 1) / sk::kSeg, ncta_g = (b.nglob + sk::kRowsPerCta - 1) / sk::kRowsPerCta;
+    b.F = dalloc<double>(ng);
+    b.fwx = dalloc<double>(ng);
+    b.fqh = dalloc<double>(ng);
+    b.fhw = dalloc<double>(ng);
+    b.fpart = dalloc<double>(std::max<int64_t>(ncta_g * s * s, nseg_g) + 64);
+    b.fcounter = dalloc<unsigned int>(cap_blocks + 8);
+    b.ftable = dalloc<double*>(cap_blocks);
+    std::vector<double*> t(cap_blocks, b.F);
+    CK(cudaMemcpyAsync(b.ftable, t.data(), sizeof(double*) * cap_blocks, cudaMemcpyHostToDevice, st));
+    CK(cudaStreamSynchronize(st));
+  }
+  void setup_nodes() {
+    const int W = P.world;
+    c.world = W;
+    c.rank = P.rank;
+    int64_t nch_max = 0;
+    for (int sd = 0; sd < nsides; ++sd) nch_max = std::max<int64_t>(nch_max, P.plan[sd].nch_max);
+    c.nch_max = nch_max;
+    c.nex = 2 * s * s;
+    std::vector<int32_t> rn(2 * W, 0);
+    for (int sd = 0; sd < 2; ++sd)
+      for (int r = 0; r < W; ++r) rn[sd * W + r] = (int32_t)P.plan[sd < nsides ? sd : 0].nch[r];
+    rank_nch = dalloc<int32_t>(2 * W);
+    CK(cudaMemcpyAsync(rank_nch, rn.data(), sizeof(int32_t) * 2 * W, cudaMemcpyHostToDevice, st));
+    CK(cudaStreamSynchronize(st));
+    c.rank_nch = rank_nch;
+    const int64_t cap = (cap_blocks + 1) * nsides * nch_max * c.nex;
+    nodes = dalloc<double>(cap);
+    gnodes = dalloc<double>(cap * W);
+    c.nodes = nodes;
+    c.gnodes = gnodes;
+  }
+  // full view: the current state, cores and coefficients; whole column blocks
+  sk::SolveConst full_view() const {
+    sk::SolveConst cf = c;
+    cf.world = 1;
+    cf.rank = 0;
+    for (int sd = 0; sd < nsides; ++sd) {
+      const SideBuf& b = side[sd];
+      sk::SideConst& f = cf.side[sd];
+      f.n = b.nglob;
+      f.nseg = (b.nglob + sk::kSeg - 1) / sk::kSeg;
+      f.ncta = (b.nglob + sk::kRowsPerCta - 1) / sk::kRowsPerCta;
+      f.row0 = 0;
+      f.dist = 0;
+      f.halo = 0;
+      f.blocks = b.ftable;
+      f.wx = b.fwx;
+      f.qh = b.fqh;
+      f.hw = b.fhw;
+      f.part = b.fpart;
+      f.counter = b.fcounter;
+    }
+    if (nsides == 1) cf.side[1] = cf.side[0];
+    return cf;
+  }
+  int64_t node_msg(int64_t nslots) const { return nslots * nsides * c.nch_max * c.nex; }
+  void gather_nodes(int64_t nslots) { P.comm->allgather(nodes, gnodes, node_msg(nslots), st); }
+  void halo_exchange() {
+    int64_t H = 0;
+    for (int sd = 0; sd < nsides; ++sd) H = std::max<int64_t>(H, side[sd].halo);
+    if (H == 0) return;
+    sk::launch_halo(c, 0, H, st);
+    sk::Comm::Halo h[2];
+    for (int sd = 0; sd < nsides; ++sd) {
+      const SideBuf& b = side[sd];
+      h[sd] = {b.hsend, b.hsend + b.halo * s, b.hrecv, b.hrecv + b.halo * s, b.halo * s};
+    }
+    P.comm->halo(h, nsides, st);
+    sk::launch_halo(c, 1, H, st);
+  }
+  sk::DevState read_state() {
+    CK(cudaStreamSynchronize(st));
+    sk::DevState hs;
+    CK(cudaMemcpy(&hs, dstate, sizeof hs, cudaMemcpyDeviceToHost));
+    return hs;
+  }
+  // whole candidate blocks of the sides in stage `want` -> full view, and back
+  bool gather_candidates(const sk::DevState& hs, int want) {
+    bool any = false;
+    for (int sd = 0; sd < nsides; ++sd) {
+      if (hs.side[sd].stage != want) continue;
+      any = true;
+      SideBuf& b = side[sd];
+      const Plan& pl = P.plan[sd];
+      std::vector<int64_t> cnt(P.world), dsp(P.world);
+      for (int r = 0; r < P.world; ++r) {
+        cnt[r] = pl.rows[r] * s;
+        dsp[r] = pl.row0[r] * s;
+      }
+      P.comm->allgatherv(b.blocks[hs.side[sd].blocks], b.F, cnt.data(), dsp.data(), st);
+    }
+    return any;
+  }
+  void scatter_candidates(const sk::DevState& hs, int want) {
+    for (int sd = 0; sd < nsides; ++sd) {
+      if (hs.side[sd].stage != want) continue;
+      SideBuf& b = side[sd];
+      CK(cudaMemcpyAsync(b.blocks[hs.side[sd].blocks], b.F + c.side[sd].row0 * s, sizeof(double) * b.n * s,
+                         cudaMemcpyDeviceToDevice, st));
+    }
+  }
+  // host-driven rare paths of a paused iteration (same order as launch_rare)
+  void rare_dist() {
+    sk::launch_dist_resume(c, st);
+    sk::DevState hs = read_state();
+    if (gather_candidates(hs, sk::ST_NEED_HH)) {
+      sk::launch_householder(full_view(), 0, st);
+      scatter_candidates(hs, sk::ST_NEED_HH);
+      hs = read_state();
+    }
+    bool clean = false;
+    int64_t kmax = 0;
+    for (int sd = 0; sd < nsides; ++sd) {
+      clean |= hs.side[sd].stage == sk::ST_NEED_CLEANUP;
+      kmax = std::max<int64_t>(kmax, hs.side[sd].blocks);
+    }
+    if (clean) {
+      sk::launch_gram_loop(c, st);
+      gather_nodes(kmax);
+      sk::launch_dist_fin(c, sk::DIST_FIN_CGRAM, node_msg(kmax), st);
+      sk::launch_update_clean(c, st);
+      gather_nodes(1);
+      sk::launch_dist_fin(c, sk::DIST_FIN_CSELF, node_msg(1), st);
+      hs = read_state();
+    }
+    if (gather_candidates(hs, sk::ST_NEED_HH2)) {
+      sk::launch_householder(full_view(), 1, st);
+      scatter_candidates(hs, sk::ST_NEED_HH2);
+    }
+  }
+  // U_0 from the full-view initialisation: local rows plus ghost rows
+  void init_dist() {
+    sk::launch_init(full_view(), P.c1, lyap ? P.c1 : P.c2, st);
+    for (int sd = 0; sd < nsides; ++sd) {
+      SideBuf& b = side[sd];
+      const int64_t r0 = c.side[sd].row0;
+      const int64_t lo = std::max<int64_t>(0, r0 - b.halo), hi = std::min<int64_t>(b.nglob, r0 + b.n + b.halo);
+      CK(cudaMemcpyAsync(b.blocks[0] + (lo - r0) * s, b.F + lo * s, sizeof(double) * (hi - lo) * s,
+                         cudaMemcpyDeviceToDevice, st));
+    }
   }
 
   void grow_cores(int64_t need) {
@@ -544,15 +780,16 @@ struct Solver {
     SideBuf& b = side[sd];
     if ((int64_t)b.blocks.size() >= need) return;
     if (need > b.cap_blocks) throw SkError(SK_ERR_CAPACITY, "basis capacity exceeded");
-    const int64_t bb = b.n * s * (int64_t)sizeof(double);
+    const int64_t stride = (b.n + 2 * b.halo) * s;  // ghost rows on both sides (row partition)
+    const int64_t bb = stride * (int64_t)sizeof(double);
     int64_t per = std::max<int64_t>(1, (int64_t(1) << 30) / std::max<int64_t>(bb, 1));
     per = std::min<int64_t>(per, b.cap_blocks - (int64_t)b.blocks.size());
     per = std::max<int64_t>(per, need - (int64_t)b.blocks.size());
-    double* chunk = dalloc<double>(per * b.n * s, false);
+    double* chunk = dalloc<double>(per * stride, b.halo > 0);
     chunks.push_back(chunk);
     const size_t first = b.blocks.size();
     for (int64_t j = 0; j < per; ++j) {
-      b.blocks.push_back(chunk + j * b.n * s);
+      b.blocks.push_back(chunk + j * stride + b.halo * s);
       b.table_host[first + j] = b.blocks.back();
     }
     // pinned source entries are written once, so the upload stays asynchronous
@@ -597,6 +834,7 @@ struct Solver {
 
   sk_solution* run() {
     setup();
+    if (dist) return run_dist();
     cudaEvent_t t0, t1;
     CK(cudaEventCreate(&t0));
     CK(cudaEventCreate(&t1));
@@ -712,9 +950,18 @@ struct Solver {
     for (auto e : pool) cudaEventDestroy(e);
     pool.clear();
 
+    return make_solution(ms, std::move(caps), std::move(cap_shape));
+  }
+
+  sk_solution* make_solution(float ms, std::vector<std::vector<double>> caps,
+                             std::vector<std::pair<int64_t, int64_t>> cap_shape) {
     auto* sol = new sk_solution();
     sol->captured = std::move(caps);
     sol->cap_shape = std::move(cap_shape);
+    if (dist) {
+      sol->row0_v = c.side[0].row0;
+      sol->row0_w = c.side[nsides > 1 ? 1 : 0].row0;
+    }
     sk::DevState hs;
     CK(cudaMemcpy(&hs, dstate, sizeof hs, cudaMemcpyDeviceToHost));
     const int64_t nrec = hs.nrec;
@@ -740,8 +987,8 @@ struct Solver {
       case sk::BREAKDOWN: sol->status = SK_SOLVE_BREAKDOWN; break;
       default: sol->status = SK_SOLVE_MAX_ITER; break;
     }
-    sol->n = P.n;
-    sol->m = lyap ? P.n : P.m;
+    sol->n = side[0].n;
+    sol->m = side[nsides > 1 ? 1 : 0].n;
     sol->s = s;
     sol->lyap = lyap;
     sol->rv = hs.rows_x;
@@ -761,6 +1008,92 @@ struct Solver {
     release(sol);
     return sol;
   }
+  // Row-partitioned CG / Lyapunov CG: per iteration two chunk-node
+  // all-gathers (one per Gram pass, both sides in one message) and one halo
+  // exchange; cores, H and the convergence test are replicated bitwise. Status
+  // is polled every `batch` iterations at the same iteration on every rank, so
+  // all ranks enqueue identical collective sequences.
+  sk_solution* run_dist() {
+    cudaEvent_t t0, t1;
+    CK(cudaEventCreate(&t0));
+    CK(cudaEventCreate(&t1));
+    sk::launch_count_reset();
+    for (int sd = 0; sd < nsides; ++sd) ensure_blocks(sd, 1);
+    CK(cudaEventRecord(t0, st));
+    init_dist();
+    sk::DevState hs0 = read_state();
+    CK(cudaGetLastError());
+    if (hs0.status == sk::RANKDEF) {
+      release(nullptr);
+      throw SkError(SK_ERR_RANK_DEFICIENT, "basis init: start block is numerically rank deficient");
+    }
+    const char* pe = getenv("SK_DIST_POLL");
+    const int64_t batch = pe ? std::max(1, atoi(pe)) : 8;
+    const int RING = 64;
+    int32_t* hstat = nullptr;
+    CK(cudaHostAlloc(&hstat, sizeof(int32_t) * RING, cudaHostAllocDefault));
+    std::vector<cudaEvent_t> rev(RING);
+    for (auto& e : rev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    auto cores = [&](int64_t k) {
+      const double rp = (double)((k + 1) * s), rq = (double)((k + 2) * s);
+      timed(4, 8.0 * 3 * rp * rp, [&] { sk::launch_cg_a(c, (k + 1) * s, st); });
+      timed(5, 8.0 * (4 * rp * rp + rq * rq), [&] { sk::launch_cg_b(c, (k + 2) * s, st); });
+    };
+    bool done = false;
+    for (int64_t k = 0; k < max_iter && !done; ++k) {
+      for (int sd = 0; sd < nsides; ++sd) ensure_blocks(sd, k + 2);
+      grow_cores((k + 2) * s);
+      timed(0, pass1_bytes(k), [&] {
+        sk::launch_lanczos_p1(c, st);
+        gather_nodes(1);
+        sk::launch_dist_fin(c, sk::DIST_FIN_P1, node_msg(1), st);
+      });
+      dbg("pass1", k);
+      timed(3, pass2_bytes(k), [&] {
+        sk::launch_lanczos_p2(c, st);
+        gather_nodes(1);
+        sk::launch_dist_fin(c, sk::DIST_FIN_P2, node_msg(1), st);
+      });
+      dbg("pass2", k);
+      sk::launch_dist_pause(c, st);
+      timed(2, 0.0, [&] { halo_exchange(); });
+      cores(k);
+      dbg("cores", k);
+      CK(cudaMemcpyAsync(&hstat[k % RING], &dstate->status, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+      CK(cudaEventRecord(rev[k % RING], st));
+      if ((k + 1) % batch == 0 || k + 1 == max_iter) {
+        CK(cudaEventSynchronize(rev[k % RING]));
+        if (hstat[k % RING] == sk::PAUSED) {
+          const int64_t kp = read_state().k;  // the paused iteration (later ones were no-ops)
+          timed(2, 0.0, [&] {
+            rare_dist();
+            halo_exchange();
+          });
+          cores(kp);
+          CK(cudaMemcpyAsync(&hstat[kp % RING], &dstate->status, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+          CK(cudaStreamSynchronize(st));
+          if (hstat[kp % RING] != sk::RUNNING && hstat[kp % RING] != sk::PAUSED) done = true;
+          k = kp;
+        } else if (hstat[k % RING] != sk::RUNNING) {
+          done = true;
+        }
+      }
+      if (P.profile) drain_events(false);
+    }
+    CK(cudaEventRecord(t1, st));
+    CK(cudaStreamSynchronize(st));
+    CK(cudaGetLastError());
+    if (P.profile) drain_events(true);
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, t0, t1));
+    cudaEventDestroy(t0);
+    cudaEventDestroy(t1);
+    for (auto& e : rev) cudaEventDestroy(e);
+    cudaFreeHost(hstat);
+    for (auto e : pool) cudaEventDestroy(e);
+    pool.clear();
+    return make_solution(ms, {}, {});
+  }
 
   // free everything except what the solution keeps (blocks + X)
   void release(sk_solution* sol) {
@@ -779,7 +1112,19 @@ struct Solver {
       dfree(b.part);
       dfree(b.counter);
       dfree(b.table);
+      dfree(b.hsend);
+      dfree(b.hrecv);
+      dfree(b.F);
+      dfree(b.fwx);
+      dfree(b.fqh);
+      dfree(b.fhw);
+      dfree(b.fpart);
+      dfree(b.fcounter);
+      dfree(b.ftable);
     }
+    dfree(rank_nch);
+    dfree(nodes);
+    dfree(gnodes);
     cudaStreamSynchronize(st);
     for (int sd = 0; sd < nsides; ++sd)
       if (side[sd].table_host) cudaFreeHost(side[sd].table_host);
@@ -841,8 +1186,21 @@ void check_device(int dev) {
   CK(cudaSetDevice(dev));
 }
 
+// rows [row0, row0 + rows) of a global CSR, column indices relative to row0
+// (negative / >= rows for ghost columns), uploaded as int32
+size_t upload_local_csr(DevCsr& d, const int64_t* rp, const int64_t* ci, const double* val, int64_t row0,
+                        int64_t rows, const StencilInfo& si, cudaStream_t st) {
+  const int64_t k0 = rp[row0], k1 = rp[row0 + rows];
+  std::vector<int64_t> lrp(rows + 1), lci(std::max<int64_t>(k1 - k0, 1));
+  for (int64_t i = 0; i <= rows; ++i) lrp[i] = rp[row0 + i] - k0;
+  for (int64_t k = k0; k < k1; ++k) lci[k - k0] = ci[k] - row0;
+  const size_t bytes = upload_csr(d, rows, k1 - k0, lrp.data(), lci.data(), val + k0, st, false);
+  d.stencil = si;
+  return bytes;
+}
+
 sk_problem* create_problem(int32_t method, const sk_csr* a, const sk_csr* b, const double* c1,
-                           const double* c2, int64_t s, const sk_gpu_options* gpu) {
+                           const double* c2, int64_t s, const sk_gpu_options* gpu, sk::Comm* comm = nullptr) {
   validate_csr(a, "A");
   const bool lyap = method == SK_METHOD_CG_LYAPUNOV;
   HostCsr bt;  // B^T: the W basis applies it (block_krylov.cpp:54-56)
@@ -889,6 +1247,31 @@ sk_problem* create_problem(int32_t method, const sk_csr* a, const sk_csr* b, con
     }
   }
   auto t0 = std::chrono::steady_clock::now();
+  if (comm && comm->size > 1) {
+    // row partition: this rank's rows of A and B^T; stencil / halo from the whole operator
+    if (method == SK_METHOD_BICGSTAB || s > 4)
+      throw SkError(SK_ERR_UNSUPPORTED, "row partition: CG / Lyapunov CG with s <= 4");
+    p->comm = comm;
+    p->world = comm->size;
+    p->rank = comm->rank;
+    const bool no_st = getenv("SK_NO_STENCIL") != nullptr;
+    for (int sd = 0; sd < (lyap ? 1 : 2); ++sd) {
+      const int64_t n = sd == 0 ? a->n_rows : bt.n_rows;
+      const int64_t* rp = sd == 0 ? a->row_ptr : bt.rp.data();
+      const int64_t* ci = sd == 0 ? a->col_idx : bt.ci.data();
+      const double* val = sd == 0 ? a->values : bt.val.data();
+      StencilInfo si;
+      if (!no_st) detect_stencil(rp, ci, val, n, si);
+      p->plan[sd] = make_plan(n, operator_halo(rp, ci, n, si), p->world);
+      p->nglob[sd] = n;
+      const Plan& pl = p->plan[sd];
+      p->h2d_bytes += upload_local_csr(p->op[sd], rp, ci, val, pl.row0[p->rank], pl.rows[p->rank], si, p->stream);
+    }
+    if (lyap) {
+      p->plan[1] = p->plan[0];
+      p->nglob[1] = p->nglob[0];
+    }
+  } else {
   p->h2d_bytes += upload_csr(p->op[0], a->n_rows, a->nnz, a->row_ptr, a->col_idx, a->values, p->stream);
   if (!lyap) {
     if (same_csr(a, bt)) {
@@ -898,6 +1281,7 @@ sk_problem* create_problem(int32_t method, const sk_csr* a, const sk_csr* b, con
       p->h2d_bytes += upload_csr(p->op[1], bt.n_rows, (int64_t)bt.val.size(), bt.rp.data(),
                                  bt.ci.data(), bt.val.data(), p->stream);
     }
+  }
   }
   CK(cudaMalloc(&p->c1, sizeof(double) * p->n * s));
   CK(cudaMemcpyAsync(p->c1, c1, sizeof(double) * p->n * s, cudaMemcpyHostToDevice, p->stream));
@@ -982,6 +1366,77 @@ sk_status sk_problem_solve(sk_problem* p, const sk_config* cfg, sk_solution** ou
 }
 
 void sk_problem_free(sk_problem* p) { destroy_problem(p); }
+
+// ---- row partition ----
+sk_status sk_partition_plan(int64_t n, int64_t halo, int32_t world, int32_t rank, sk_partition* out) {
+  return run_guarded([&] {
+    if (!out || rank < 0 || rank >= world) throw SkError(SK_ERR_DIMENSION, "sk_partition_plan: bad rank / output");
+    const Plan p = make_plan(n, halo, world);
+    out->row0 = p.row0[rank];
+    out->rows = p.rows[rank];
+    out->chunk_rows = p.chunk_rows;
+    out->chunks = p.nch[rank];
+    out->chunks_max = p.nch_max;
+    out->chunks_total = p.total;
+    out->halo = p.halo;
+  });
+}
+sk_status sk_nccl_unique_id(uint8_t* out128) {
+  return run_guarded([&] {
+    try {
+      sk::nccl_unique_id(out128);
+    } catch (const std::runtime_error& e) {
+      throw SkError(SK_ERR_CUDA, e.what());
+    }
+  });
+}
+sk_status sk_comm_create_nccl(const uint8_t* id128, int32_t nranks, int32_t rank, int32_t device, sk_comm** out) {
+  if (out) *out = nullptr;
+  return run_guarded([&] {
+    auto c = std::make_unique<sk_comm>();
+    try {
+      c->impl.reset(sk::make_nccl_comm(id128, nranks, rank, device));
+    } catch (const std::runtime_error& e) {
+      throw SkError(SK_ERR_CUDA, e.what());
+    }
+    *out = c.release();
+  });
+}
+sk_status sk_comm_create_local_group(int32_t nranks, sk_comm** out) {
+  return run_guarded([&] {
+    std::vector<sk::Comm*> cs(nranks > 0 ? nranks : 1, nullptr);
+    try {
+      sk::make_local_group(nranks, cs.data());
+    } catch (const std::runtime_error& e) {
+      throw SkError(SK_ERR_DIMENSION, e.what());
+    }
+    for (int r = 0; r < nranks; ++r) {
+      out[r] = new sk_comm();
+      out[r]->impl.reset(cs[r]);
+    }
+  });
+}
+int32_t sk_comm_rank(const sk_comm* c) { return c ? c->impl->rank : -1; }
+int32_t sk_comm_size(const sk_comm* c) { return c ? c->impl->size : -1; }
+void sk_comm_free(sk_comm* c) { delete c; }
+sk_status sk_problem_create_partitioned(int32_t method, const sk_csr* a, const sk_csr* b, const double* c1,
+                                        const double* c2, int64_t s, const sk_gpu_options* gpu, sk_comm* comm,
+                                        sk_problem** out) {
+  if (out) *out = nullptr;
+  return run_guarded([&] {
+    if (!comm) throw SkError(SK_ERR_DIMENSION, "sk_problem_create_partitioned: null communicator");
+    *out = create_problem(method, a, b, c1, c2, s, gpu, comm->impl.get());
+  });
+}
+sk_status sk_solution_partition(const sk_solution* sol, int64_t* row0_v, int64_t* rows_v, int64_t* row0_w,
+                                int64_t* rows_w) {
+  if (!sol) return SK_ERR_DIMENSION;
+  if (row0_v) *row0_v = sol->row0_v;
+  if (rows_v) *rows_v = sol->n;
+  if (row0_w) *row0_w = sol->row0_w;
+  if (rows_w) *rows_w = sol->m;
+  return SK_OK;
+}
 
 int32_t sk_solution_status(const sk_solution* sol) { return sol ? sol->status : -1; }
 void sk_solution_dims(const sk_solution* sol, int64_t* n, int64_t* rv, int64_t* m, int64_t* rw) {

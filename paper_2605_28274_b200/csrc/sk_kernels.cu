@@ -439,21 +439,22 @@ __device__ __forceinline__ void stencil_row(const SideConst& sc, const double* _
                                             double* acc, double* own) {
   constexpr int K = DIM == 2 ? 5 : 7;
   constexpr int C = DIM == 2 ? 2 : 3;
-  const int i = (int)i64;
+  const int i = (int)i64;              // local row (addressing; halo rows at i < 0, i >= n)
+  const int gi = i + (int)sc.row0;     // global row (grid coordinates)
   const int g = (int)sc.sg;
   int ix, iy, iz = 0;
   if (POW2) {
     const int sh = sc.sg_pow2;
-    ix = i & (g - 1);
+    ix = gi & (g - 1);
     if (DIM == 2) {
-      iy = i >> sh;
+      iy = gi >> sh;
     } else {
-      iy = (i >> sh) & (g - 1);
-      iz = i >> (2 * sh);
+      iy = (gi >> sh) & (g - 1);
+      iz = gi >> (2 * sh);
     }
   } else {
-    const int r = i / g;
-    ix = i - r * g;
+    const int r = gi / g;
+    ix = gi - r * g;
     if (DIM == 2) {
       iy = r;
     } else {
@@ -563,7 +564,7 @@ __device__ __forceinline__ double tree32(double* a) {
 // aligned groups of 32 in registers, then the group nodes in smem.
 template <int NE>
 __device__ void final_tree(const double* part, int64_t P, double* out) {
-  constexpr int MAXG = 128;
+  constexpr int MAXG = NE <= 16 ? 128 : 32;  // static smem bound for large s
   __shared__ double gnode[NE][MAXG];
   const int64_t ngroups = (P + 31) / 32;
   if (ngroups > MAXG) {
@@ -620,6 +621,43 @@ __device__ __forceinline__ void warp_seg_to_cta(const double* acc, int nvalid_ct
     for (int w = 0; w < kFusedSegsPerCta; ++w) a[w] = snode[w][e];
     part_out[e] = tree_reduce_local(a, nvalid_cta);
   }
+}
+
+// =====================================================================
+// Row partition. Rank boundaries sit on reduction chunks: aligned
+// power-of-two groups of R1 segments (>= 32), so a chunk node is a node of the
+// canonical tree and the canonical tree over all ranks' chunk nodes, in global
+// order, is bitwise the single-GPU root. The last CTA of a partitioned pass
+// writes its chunk nodes; after the all-gather, k_dist_fin forms the root and
+// runs the same finalisation as the single-GPU last CTA.
+// Node (slot, side, chunk j) lives at ((slot * nsides + side) * nch_max + j) * nex.
+// =====================================================================
+__device__ __forceinline__ int64_t node_off(const SolveConst& c, int64_t slot, int side, int64_t j) {
+  return ((slot * c.nsides + side) * c.nch_max + j) * c.nex;
+}
+template <int NE>
+__device__ void dist_emit(const SolveConst& c, int side, int64_t slot, const double* part, int64_t ncta,
+                          int64_t chunk) {
+  const SideConst& sc = c.side[side];
+  for (int64_t j = 0; j < sc.nch; ++j) {
+    const int64_t p0 = j * chunk;
+    final_tree<NE>(part + p0 * NE, mn64(chunk, ncta - p0), c.nodes + node_off(c, slot, side, j));
+  }
+}
+// canonical tree over every rank's chunk nodes (all threads call; result in out)
+template <int NE>
+__device__ void dist_root(const SolveConst& c, int side, int64_t slot, int64_t msg, double* out) {
+  for (int e = threadIdx.x; e < NE; e += blockDim.x) {
+    TreeStream ts;
+    ts.init();
+    for (int r = 0; r < c.world; ++r) {
+      const double* base = c.gnodes + r * msg + node_off(c, slot, side, 0) + e;
+      const int nr = c.rank_nch[side * c.world + r];
+      for (int j = 0; j < nr; ++j) ts.push(__ldcg(base + (int64_t)j * c.nex));
+    }
+    out[e] = ts.finish();
+  }
+  __syncthreads();
 }
 
 // =====================================================================
@@ -789,6 +827,47 @@ __device__ __forceinline__ void p1_dispatch(const SideConst& sc, const double* _
   }
 }
 
+// pass-1 root -> c_b, M_b for blocks k-2 (if any) and k-1
+template <int S>
+__device__ void p1_finish(const SideConst& sc, int64_t k, const double* res) {
+  constexpr int NB = S * S;
+  if (threadIdx.x < 2) {
+    const int slot = threadIdx.x;  // 0: block k-2, 1: block k-1
+    if (slot == 1 || k >= 2) {
+      const int64_t b = slot == 0 ? k - 2 : k - 1;
+      double cb[NB], mb[NB];
+      block_coefs(sc.nfac + b * (NB + S), res + slot * NB, S, cb, mb);
+      for (int e = 0; e < NB; ++e) {
+        sc.coef[b * NB + e] = cb[e];
+        sc.mcoef[b * NB + e] = mb[e];
+      }
+    }
+  }
+}
+// self-Gram root -> gbase (symmetric), then finalisation
+template <int S>
+__device__ void gram_finish(const SolveConst& c, int side, const double* res, int how) {
+  constexpr int NS = S * (S + 1) / 2;
+  SideState& sst = c.st->side[side];
+  for (int e = threadIdx.x; e < NS; e += blockDim.x) {
+    int t, u;
+    unpack_tri(e, t, u);
+    sst.gbase[u * S + t] = res[e];
+    sst.gbase[t * S + u] = res[e];
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    if (how == 2) {
+      finalize_init(c, side);
+    } else if (how == 1) {
+      sst.paths[2]++;
+      finalize_direct(c, side, false);
+    } else {
+      finalize_direct(c, side, true);
+    }
+  }
+}
+
 // Lanczos pass 1: w = (op U_{k-1}) N_{k-1}^{-1}; G = U_{k-2}^T w, U_{k-1}^T w
 // (block_krylov.cpp:71-84, CGS form). w is stored only for CSR operators.
 template <int S>
@@ -832,20 +911,13 @@ __global__ void __launch_bounds__(256, 4) k_lanczos_p1(SolveConst c) {
   }
   warp_seg_to_cta<NE>(acc, nvalid_cta, sc.part + cta * NE);
   if (!last_cta_arrive(sc.counter + 0, (unsigned)ncta)) return;
+  if (sc.dist) {
+    dist_emit<NE>(c, side, 0, sc.part, ncta, sc.chunk_f);
+    return;
+  }
   __shared__ double res[NE];
   final_tree<NE>(sc.part, ncta, res);
-  if (threadIdx.x < 2) {
-    const int slot = threadIdx.x;  // 0: block k-2, 1: block k-1
-    if (slot == 1 || two) {
-      const int64_t b = slot == 0 ? k - 2 : k - 1;
-      double cb[NB], mb[NB];
-      block_coefs(sc.nfac + b * (NB + S), res + slot * NB, S, cb, mb);
-      for (int e = 0; e < NB; ++e) {
-        sc.coef[b * NB + e] = cb[e];
-        sc.mcoef[b * NB + e] = mb[e];
-      }
-    }
-  }
+  p1_finish<S>(sc, k, res);
 }
 
 template <int S, int MODE, bool TWO, bool CHECK>
@@ -956,17 +1028,13 @@ __global__ void __launch_bounds__(256, 5) k_lanczos_p2(SolveConst c) {
   }
   warp_seg_to_cta<NS>(acc, nvalid_cta, sc.part + cta * NS);
   if (!last_cta_arrive(sc.counter + 1, (unsigned)ncta)) return;
+  if (sc.dist) {
+    dist_emit<NS>(c, side, 0, sc.part, ncta, sc.chunk_f);
+    return;
+  }
   __shared__ double res[NS];
   final_tree<NS>(sc.part, ncta, res);
-  SideState& sst = c.st->side[side];
-  for (int e = threadIdx.x; e < NS; e += blockDim.x) {
-    int t, u;
-    unpack_tri(e, t, u);
-    sst.gbase[u * S + t] = res[e];
-    sst.gbase[t * S + u] = res[e];
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) finalize_direct(c, side, true);
+  gram_finish<S>(c, side, res, 0);
 }
 
 // Clean-up Gram (rare path): each CTA sweeps all blocks for its row group, so
@@ -1017,6 +1085,10 @@ __global__ void __launch_bounds__(256) k_gram_loop(SolveConst c) {
     __syncthreads();
   }
   if (!last_cta_arrive(sc.counter + 2, (unsigned)sc.ncta)) return;
+  if (sc.dist) {
+    for (int64_t b = 0; b < k; ++b) dist_emit<NB>(c, side, b, sc.part + b * sc.ncta * NB, sc.ncta, sc.chunk_g);
+    return;
+  }
   for (int64_t b = threadIdx.x; b < k; b += blockDim.x) {
     double G[NB], cb[NB], mb[NB];
     for (int e = 0; e < NB; ++e) G[e] = tree_stream(sc.part + b * sc.ncta * NB + e, sc.ncta, NB);
@@ -1029,13 +1101,19 @@ __global__ void __launch_bounds__(256) k_gram_loop(SolveConst c) {
 }
 
 // =====================================================================
-// Arnoldi update (many blocks): one thread per (row, column) chain,
-// y(i,u) = x(i,u) - sum_b [sum_t U_b(i,t) M_b(t,u)] in ascending b (same
-// arithmetic as k_update); M and the block pointers staged in smem per chunk.
+// Arnoldi update (many blocks): one thread per row carrying its S column
+// chains, y(i,u) = x(i,u) - sum_b [sum_t U_b(i,t) M_b(t,u)] in ascending b
+// (same arithmetic per chain as k_update); M and the block pointers staged in
+// smem per chunk, 8 block rows in flight per thread.
 // =====================================================================
+constexpr int kArnThreads = 128;
+__device__ __forceinline__ const double* blk_ptr(const SideConst& sc, int64_t b) {
+  return reinterpret_cast<const double*>(__ldg(reinterpret_cast<const unsigned long long*>(sc.blocks) + b));
+}
 template <int S>
-__global__ void __launch_bounds__(256) k_arn_update(SolveConst c, int mode) {
-  constexpr int CH = 64;
+__global__ void __launch_bounds__(kArnThreads) k_arn_update(SolveConst c, int mode) {
+  constexpr int UN = 8;
+  constexpr int CH = (S <= 2 ? 1024 : 4096 / (S * S));  // M chunk (blocks), multiple of UN
   const int side = blockIdx.y;
   if (side >= c.nsides) return;
   const DevState* st = c.st;
@@ -1049,31 +1127,49 @@ __global__ void __launch_bounds__(256) k_arn_update(SolveConst c, int mode) {
   const double* mc = mode == UM_FIRST ? sc.mcoef : sc.mcoef2;
   const int64_t b0 = mode == UM_FIRST ? first_block(c, k) : 0, b1 = k;
   const int64_t n = sc.n;
+  if ((int64_t)blockIdx.x * blockDim.x >= n) return;
   const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if ((int64_t)blockIdx.x * blockDim.x >= n * S) return;
-  const bool active = g < n * S;
-  const int64_t i = active ? g / S : n - 1;
-  const int u = (int)(g % S);
-  __shared__ double Ms[CH][S * S];
-  __shared__ const double* Bp[CH];
-  double y = __ldcg(xin + i * S + u);
-  for (int64_t cb = b0; cb < b1; cb += CH) {
-    const int nb = (int)mn64(CH, b1 - cb);
-    __syncthreads();
-    for (int e = threadIdx.x; e < nb * S * S; e += blockDim.x) Ms[e / (S * S)][e % (S * S)] = __ldcg(mc + (cb + e / (S * S)) * S * S + e % (S * S));
-    for (int e = threadIdx.x; e < nb; e += blockDim.x) Bp[e] = sc.blocks[cb + e];
-    __syncthreads();
-#pragma unroll 4
-    for (int b = 0; b < nb; ++b) {
-      double a[S];
-      ld_raw<S>(Bp[b], i, a);
-      double tmp = 0.0;
+  const bool active = g < n;
+  const int64_t i = active ? g : n - 1;
+  __shared__ double Ms[CH * S * S];
+  double y[S];
+  ld_raw_cg<S>(xin, i, y);
+  double cur[UN][S], nxt[UN][S];
 #pragma unroll
-      for (int t = 0; t < S; ++t) tmp = __dadd_rn(tmp, __dmul_rn(a[t], Ms[b][u * S + t]));
-      y = __dsub_rn(y, tmp);
+  for (int q = 0; q < UN; ++q)
+    if (b0 + q < b1) ld_raw<S>(blk_ptr(sc, b0 + q), i, cur[q]);
+  int64_t cb = b0 - CH;  // chunk base of the staged M
+  for (int64_t bb = b0; bb < b1; bb += UN) {
+    if (bb >= cb + CH) {  // restage M (uniform across the CTA)
+      cb = bb;
+      const int nb = (int)mn64(CH, b1 - cb);
+      __syncthreads();
+      for (int e = threadIdx.x; e < nb * S * S; e += blockDim.x) Ms[e] = __ldcg(mc + cb * S * S + e);
+      __syncthreads();
     }
+    // prefetch the next group while this one computes
+#pragma unroll
+    for (int q = 0; q < UN; ++q)
+      if (bb + UN + q < b1) ld_raw<S>(blk_ptr(sc, bb + UN + q), i, nxt[q]);
+    const double* m = Ms + (bb - cb) * S * S;
+#pragma unroll
+    for (int q = 0; q < UN; ++q) {
+      if (bb + q < b1) {
+#pragma unroll
+        for (int u = 0; u < S; ++u) {
+          double tmp = 0.0;
+#pragma unroll
+          for (int t = 0; t < S; ++t) tmp = __dadd_rn(tmp, __dmul_rn(cur[q][t], m[q * S * S + u * S + t]));
+          y[u] = __dsub_rn(y[u], tmp);
+        }
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < UN; ++q)
+#pragma unroll
+      for (int t = 0; t < S; ++t) cur[q][t] = nxt[q][t];
   }
-  if (active) xout[i * S + u] = y;
+  if (active) st_row<S>(xout, i, y);
 }
 
 // R1 self Gram x^T x of the candidate U_k (one warp per segment) + finalise.
@@ -1246,25 +1342,14 @@ __global__ void __launch_bounds__(256) k_update(SolveConst c, int mode) {
   if (!gram) return;
   cta_combine<NS>(segv, g.nvalid_warp, g.nvalid_cta, sc.part + cta * NS);
   if (!last_cta_arrive(sc.counter + 1, (unsigned)sc.ncta)) return;
-  SideState& sst = c.st->side[side];
-  for (int e = threadIdx.x; e < NS; e += blockDim.x) {
-    const double v = tree_stream(sc.part + e, sc.ncta, NS);
-    int t, u;
-    unpack_tri(e, t, u);
-    sst.gbase[u * S + t] = v;
-    sst.gbase[t * S + u] = v;
+  if (sc.dist) {
+    dist_emit<NS>(c, side, 0, sc.part, sc.ncta, sc.chunk_g);
+    return;
   }
+  __shared__ double res[NS];
+  for (int e = threadIdx.x; e < NS; e += blockDim.x) res[e] = tree_stream(sc.part + e, sc.ncta, NS);
   __syncthreads();
-  if (threadIdx.x == 0) {
-    if (mode == UM_INIT) {
-      finalize_init(c, side);
-    } else if (mode == UM_CLEAN) {
-      sst.paths[2]++;
-      finalize_direct(c, side, false);
-    } else {
-      finalize_direct(c, side, true);
-    }
-  }
+  gram_finish<S>(c, side, res, mode == UM_INIT ? 2 : (mode == UM_CLEAN ? 1 : 0));
 }
 
 // =====================================================================
@@ -1766,6 +1851,86 @@ __global__ void k_export_block(const double* blk, const double* nfac, int64_t b,
   }
 }
 
+// =====================================================================
+// Row partition: finalisation from the all-gathered chunk nodes (one CTA per
+// side; the guards are those of the last CTA it replaces), the pause that hands
+// a rare path to the host, and the halo exchange staging of the newest block.
+// =====================================================================
+enum DistFin : int { DF_P1 = 0, DF_P2 = 1, DF_CGRAM = 2, DF_CSELF = 3 };
+template <int S>
+__global__ void __launch_bounds__(256) k_dist_fin(SolveConst c, int mode, int64_t msg) {
+  constexpr int NB = S * S, NE = 2 * NB, NS = S * (S + 1) / 2;
+  const int side = blockIdx.x;
+  if (side >= c.nsides) return;
+  DevState* st = c.st;
+  if (st->status != RUNNING) return;
+  const SideState& ss = st->side[side];
+  const SideConst& sc = c.side[side];
+  const int64_t k = ss.blocks;
+  if (mode == DF_P1 || mode == DF_P2) {
+    if (ss.exhausted || ss.broken) return;
+  } else if (ss.stage != ST_NEED_CLEANUP) {
+    return;
+  }
+  __shared__ double res[NE];
+  if (mode == DF_P1) {
+    dist_root<NE>(c, side, 0, msg, res);
+    p1_finish<S>(sc, k, res);
+  } else if (mode == DF_P2 || mode == DF_CSELF) {
+    dist_root<NS>(c, side, 0, msg, res);
+    gram_finish<S>(c, side, res, mode == DF_CSELF ? 1 : 0);
+  } else {
+    for (int64_t b = threadIdx.x; b < k; b += blockDim.x) {
+      double G[NB], cb[NB], mb[NB];
+      for (int e = 0; e < NB; ++e) {
+        TreeStream ts;
+        ts.init();
+        for (int r = 0; r < c.world; ++r) {
+          const double* base = c.gnodes + r * msg + node_off(c, b, side, 0) + e;
+          for (int j = 0; j < c.rank_nch[side * c.world + r]; ++j) ts.push(__ldcg(base + (int64_t)j * c.nex));
+        }
+        G[e] = ts.finish();
+      }
+      block_coefs(sc.nfac + b * (NB + S), G, S, cb, mb);
+      for (int e = 0; e < NB; ++e) {
+        sc.coef2[b * NB + e] = cb[e];
+        sc.mcoef2[b * NB + e] = mb[e];
+      }
+    }
+  }
+}
+
+// newest block's first / last `halo` local rows -> hsend (lo | hi)
+template <int S>
+__global__ void k_halo_pack(SolveConst c) {
+  const int side = blockIdx.y;
+  if (side >= c.nsides) return;
+  const SideConst& sc = c.side[side];
+  const int64_t H = sc.halo;
+  const int64_t kb = c.st->side[side].blocks;
+  if (H == 0 || kb < 1) return;
+  const double* src = sc.blocks[kb - 1];
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < H * S; e += (int64_t)gridDim.x * blockDim.x) {
+    sc.hsend[e] = src[e];
+    sc.hsend[H * S + e] = src[(sc.n - H) * S + e];
+  }
+}
+// hrecv (from previous | next rank) -> ghost rows of the newest block
+template <int S>
+__global__ void k_halo_unpack(SolveConst c) {
+  const int side = blockIdx.y;
+  if (side >= c.nsides) return;
+  const SideConst& sc = c.side[side];
+  const int64_t H = sc.halo;
+  const int64_t kb = c.st->side[side].blocks;
+  if (H == 0 || kb < 1) return;
+  double* dst = sc.blocks[kb - 1];
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < H * S; e += (int64_t)gridDim.x * blockDim.x) {
+    if (c.rank > 0) dst[e - H * S] = sc.hrecv[e];
+    if (c.rank < c.world - 1) dst[sc.n * S + e] = sc.hrecv[H * S + e];
+  }
+}
+
 static int rows_grid(int64_t n) {
   int64_t g = (n + 255) / 256;
   if (g > 148 * 16) g = 148 * 16;
@@ -1800,6 +1965,8 @@ struct Launch {
                          double* y, int64_t n, cudaStream_t st);
   static void export_block(const double* blk, const double* nfac, int64_t b, double* out, int64_t n,
                            cudaStream_t st);
+  static void dist_fin(const SolveConst& c, int mode, int64_t msg, cudaStream_t st);
+  static void halo(const SolveConst& c, int unpack, int64_t H, cudaStream_t st);
 };
 #else
 template <int S>
@@ -1829,11 +1996,21 @@ struct Launch {
   static void householder(const SolveConst& c, int which, cudaStream_t st) {
     k_householder<S><<<c.nsides, 1024, 0, st>>>(c, which);
   }
+  static void dist_fin(const SolveConst& c, int mode, int64_t msg, cudaStream_t st) {
+    k_dist_fin<S><<<c.nsides, 256, 0, st>>>(c, mode, msg);
+  }
+  static void halo(const SolveConst& c, int unpack, int64_t H, cudaStream_t st) {
+    const unsigned g = (unsigned)((H * S + 255) / 256 > 0 ? ((H * S + 255) / 256 < 1184 ? (H * S + 255) / 256 : 1184) : 1);
+    if (unpack)
+      k_halo_unpack<S><<<dim3(g, c.nsides), 256, 0, st>>>(c);
+    else
+      k_halo_pack<S><<<dim3(g, c.nsides), 256, 0, st>>>(c);
+  }
   static void arn_update(const SolveConst& c, int mode, cudaStream_t st) {
     int64_t nmax, cmax;
     dims(c, nmax, cmax);
-    const unsigned g = (unsigned)((nmax * S + 255) / 256);
-    k_arn_update<S><<<dim3(g, c.nsides), 256, 0, st>>>(c, mode);
+    const unsigned g = (unsigned)((nmax + kArnThreads - 1) / kArnThreads);
+    k_arn_update<S><<<dim3(g, c.nsides), kArnThreads, 0, st>>>(c, mode);
   }
   static void self_gram(const SolveConst& c, cudaStream_t st) {
     k_self_gram<S><<<dim3(fused_grid(c), 1, c.nsides), 256, 0, st>>>(c, 0);
@@ -2383,6 +2560,45 @@ void launch_rare(const SolveConst& c, int64_t kmax_blocks, cudaStream_t st) {
   SK_DISPATCH_S(c.s, update(c, (int)UM_CLEAN, st));
   SK_DISPATCH_S(c.s, householder(c, 1, st));
   g_launches += 4;
+}
+static __global__ void k_dist_pause(SolveConst c) {
+  DevState* st = c.st;
+  if (threadIdx.x != 0 || st->status != RUNNING) return;
+  for (int sd = 0; sd < c.nsides; ++sd) {
+    const int g = st->side[sd].stage;
+    if (g == ST_NEED_HH || g == ST_NEED_CLEANUP) st->status = PAUSED;
+  }
+}
+static __global__ void k_dist_resume(SolveConst c) {
+  if (threadIdx.x == 0 && c.st->status == PAUSED) c.st->status = RUNNING;
+}
+void launch_dist_fin(const SolveConst& c, int mode, int64_t msg, cudaStream_t st) {
+  SK_DISPATCH_S(c.s, dist_fin(c, mode, msg, st));
+  g_launches += 1;
+}
+void launch_dist_pause(const SolveConst& c, cudaStream_t st) {
+  k_dist_pause<<<1, 32, 0, st>>>(c);
+  g_launches += 1;
+}
+void launch_dist_resume(const SolveConst& c, cudaStream_t st) {
+  k_dist_resume<<<1, 32, 0, st>>>(c);
+  g_launches += 1;
+}
+void launch_halo(const SolveConst& c, int unpack, int64_t H, cudaStream_t st) {
+  SK_DISPATCH_S(c.s, halo(c, unpack, H, st));
+  g_launches += 1;
+}
+void launch_householder(const SolveConst& c, int which, cudaStream_t st) {
+  SK_DISPATCH_S(c.s, householder(c, which, st));
+  g_launches += 1;
+}
+void launch_gram_loop(const SolveConst& c, cudaStream_t st) {
+  SK_DISPATCH_S(c.s, gram_loop(c, st));
+  g_launches += 1;
+}
+void launch_update_clean(const SolveConst& c, cudaStream_t st) {
+  SK_DISPATCH_S(c.s, update(c, (int)UM_CLEAN, st));
+  g_launches += 1;
 }
 void launch_arnoldi_ext(const SolveConst& c, int64_t kmax_blocks, cudaStream_t st) {
   SK_DISPATCH_S(c.s, spmm(c, st));

@@ -23,6 +23,15 @@ void launch_cg_a(const SolveConst& c, int64_t rmax, cudaStream_t st);
 void launch_cg_b(const SolveConst& c, int64_t rmax, cudaStream_t st);
 void launch_spmm_plain(int s, const int32_t* rp, const int32_t* ci, const double* val,
                        const double* x, double* y, int64_t n, cudaStream_t st);
+// row partition (world > 1)
+enum { DIST_FIN_P1 = 0, DIST_FIN_P2 = 1, DIST_FIN_CGRAM = 2, DIST_FIN_CSELF = 3 };
+void launch_dist_fin(const SolveConst& c, int mode, int64_t msg, cudaStream_t st);
+void launch_dist_pause(const SolveConst& c, cudaStream_t st);
+void launch_dist_resume(const SolveConst& c, cudaStream_t st);
+void launch_halo(const SolveConst& c, int unpack, int64_t H, cudaStream_t st);
+void launch_householder(const SolveConst& c, int which, cudaStream_t st);
+void launch_gram_loop(const SolveConst& c, cudaStream_t st);
+void launch_update_clean(const SolveConst& c, cudaStream_t st);
 void launch_block_to_colmajor(const double* blk, double* out, int64_t n, int s, cudaStream_t st);
 void launch_colmajor_to_block(const double* in, double* blk, int64_t n, int s, cudaStream_t st);
 }  // namespace sk

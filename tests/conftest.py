@@ -29,3 +29,12 @@ def po():
     from oracle import pyoracle
     pyoracle.build()
     return pyoracle
+
+
+@pytest.fixture(scope="session")
+def sk_host():
+    """The library for host-only entry points (no device needed)."""
+    import paper_2605_28274_b200 as sk
+    from paper_2605_28274_b200 import build
+    build.build()
+    return sk
