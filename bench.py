@@ -14,6 +14,12 @@ bases per solve) are far larger than the 126 MB L2. value = iterations / s
 (max over ranks). e2e = the same metric through sk_factorized_cg with host
 buffers (host validation + transposition + H2D + solve + D2H of history and core).
 
+--gpus N > 1 (torchrun, one rank per GPU): CG / Lyapunov CG configs run the
+row-partitioned solve over NCCL -- each rank holds 1/N of the rows
+of A, B and the bases; per iteration two chunk-node all-gathers and one halo
+exchange; the same total problem at every N ("scaling": "strong"), value = the
+solve's iterations / s (max over ranks). BiCGSTAB configs run N replicas.
+
 --impl reference: the reference's algorithm on the host cores (the reference
 itself cannot be built here -- Eigen3/GTest/vendor headers absent -- so its C
 restatement in oracle/, reference-order mode, parallel SpMM), on a bounded
@@ -207,7 +213,15 @@ def main():
     cfg = baseline_config(args.config)
     scfg = sk.SolverConfig(eps_tol=cfg.eps_tol, max_iter=cfg.max_iter)
     gpu = sk.GpuOptions(device=local, profile=True)
-    prob = sk.ResidentProblem(cfg.method, cfg.a, cfg.b, cfg.c1, cfg.c2, gpu=gpu)
+    partitioned = world > 1 and cfg.method in ("cg", "cg_lyapunov")
+    comm = None
+    if partitioned:
+        uid = [sk.Communicator.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        comm = sk.Communicator.nccl(uid[0], world, rank, local)
+        prob = sk.PartitionedProblem(cfg.method, cfg.a, cfg.b, cfg.c1, cfg.c2, comm, gpu=gpu)
+    else:
+        prob = sk.ResidentProblem(cfg.method, cfg.a, cfg.b, cfg.c1, cfg.c2, gpu=gpu)
 
     for _ in range(args.warmup):
         sol = prob.solve(scfg)
@@ -239,7 +253,7 @@ def main():
     prob.free()
 
     dev_max = max_over_ranks(dev_s, dist, local)
-    total_iters = iters * world
+    total_iters = iters if partitioned else iters * world
     value = total_iters / dev_max
     peak, peak_src = peaks()
     dom = max(classes.items(), key=lambda kv: kv[1]["time_s"])
@@ -252,12 +266,14 @@ def main():
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1e3 * dev_max / args.steps, "higher_is_better": True,
-        "scaling": "weak" if world > 1 else "weak", "vs_baseline": None, "dtype": "f64",
+        "scaling": "strong" if partitioned else "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded random_rhs N(0,1) blocks, stencil operators; BASELINE.json configs)",
         "config": {"workload": f"{cfg.name}: {cfg.description}", "n": cfg.a.n_rows,
                    "s": int(cfg.c1.shape[1]), "iterations_per_step": iters // max(args.steps, 1),
                    "final_rel_residual": hist.final_rel_residual() if hist else None,
-                   "status": status, "parallelism": f"replicas x{world}" if world > 1 else "1 GPU",
+                   "status": status,
+                   "parallelism": (f"row partition x{world} (NCCL all-gather + halo)" if partitioned
+                                   else (f"replicas x{world}" if world > 1 else "1 GPU")),
                    "l2": "inputs larger than L2 (CSR 1.07 GB + 108 GB bases per solve at C5)",
                    "wall_s_timed_region": wall},
         "roofline": {"bound": "hbm", "kernel": dom[0], "achieved": achieved, "peak": peak,
@@ -270,7 +286,28 @@ def main():
         "gpu_launches": launches,
     }
 
-    if rank == 0 and not args.no_e2e:
+    if partitioned and not args.no_e2e:
+        # every rank: host buffers -> its rows on the device -> solve -> core to host
+        e2e_its, e2e_s, h2d, d2h = 0, 0.0, 0, 0
+        for _ in range(args.e2e_steps):
+            barrier_sync(dist, local)
+            t0 = time.perf_counter()
+            p2 = sk.PartitionedProblem(cfg.method, cfg.a, cfg.b, cfg.c1, cfg.c2, comm, gpu=sk.GpuOptions(device=local))
+            sol = p2.solve(scfg)
+            core = sol.core
+            dt = max_over_ranks(time.perf_counter() - t0, dist, local)
+            e2e_s += dt
+            e2e_its += sol.history.iterations()
+            h2d += sol.stats["h2d_bytes"]
+            d2h += sol.stats["d2h_bytes"] + core.nbytes
+            sol.free()
+            p2.free()
+        line["e2e"] = {"value": e2e_its / e2e_s, "unit": UNIT,
+                       "h2d_bytes_per_step": h2d // args.e2e_steps,
+                       "d2h_bytes_per_step": d2h // args.e2e_steps,
+                       "note": "per rank (rank 0's bytes); wall time max over ranks; includes host "
+                               "CSR checks/transposition and the local-row upload"}
+    if rank == 0 and not partitioned and not args.no_e2e:
         e2e_its, e2e_s, h2d, d2h = 0, 0.0, 0, 0
         for _ in range(args.e2e_steps):
             t0 = time.perf_counter()
@@ -302,6 +339,8 @@ def main():
             line["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": 1, "kind": "port", "sample": str(e)}
     if rank == 0:
         print(json.dumps(line), flush=True)
+    if comm is not None:
+        comm.free()
     if dist is not None:
         dist.destroy_process_group()
 

@@ -470,7 +470,7 @@ struct Solver {
     c.tol = cfg.breakdown_tol;
     c.eps = cfg.eps_tol;
     c.max_iter = max_iter;
-    dist = P.world > 1;
+    dist = P.comm != nullptr;
     if (dist && (arnoldi || !sk::lanczos_fused_ok(c)))
       throw SkError(SK_ERR_UNSUPPORTED, "row partition: CG / Lyapunov CG with s <= 4 (no full reorthogonalisation)");
     for (int sd = 0; sd < nsides; ++sd) {
@@ -1247,7 +1247,7 @@ sk_problem* create_problem(int32_t method, const sk_csr* a, const sk_csr* b, con
     }
   }
   auto t0 = std::chrono::steady_clock::now();
-  if (comm && comm->size > 1) {
+  if (comm) {
     // row partition: this rank's rows of A and B^T; stencil / halo from the whole operator
     if (method == SK_METHOD_BICGSTAB || s > 4)
       throw SkError(SK_ERR_UNSUPPORTED, "row partition: CG / Lyapunov CG with s <= 4");

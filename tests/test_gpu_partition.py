@@ -137,3 +137,23 @@ def test_partitioned_rejects_bicgstab(sk, po):
     comms = sk.Communicator.local_group(2)
     with pytest.raises(sk.UnsupportedError):
         sk.PartitionedProblem("bicgstab", a, a, c, c, comms[0])
+
+
+@pytest.mark.parametrize("transport", ["local", "nccl"])
+def test_partitioned_single_rank_transports(sk, po, transport):
+    """One-rank communicator: the partitioned data path (chunk nodes, all-gather,
+    replicated finalisation) through each transport, incl. NCCL loaded at run time."""
+    a = to_sk(sk, po.laplacian_2d(128))
+    c1, c2 = po.random_rhs(a.n_rows, 2, 31), po.random_rhs(a.n_rows, 2, 32)
+    cfg = sk.SolverConfig(eps_tol=1e-8, max_iter=20)
+    ref = sk.factorized_cg(a, a, c1, c2, cfg)
+    if transport == "nccl":
+        comm = sk.Communicator.nccl(sk.Communicator.nccl_unique_id(), 1, 0, 0)
+    else:
+        comm = sk.Communicator.local_group(1)[0]
+    prob = sk.PartitionedProblem("cg", a, a, c1, c2, comm)
+    sol = prob.solve(cfg)
+    _check([sol], ref)
+    sol.free()
+    prob.free()
+    comm.free()
