@@ -17,6 +17,7 @@ import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libsk_b200.so")
+LIB_PATH = os.environ.get("SK_LIB_PATH", LIB_PATH)  # experiment variants (build.py SK_VARIANT)
 
 i64p = C.POINTER(C.c_int64)
 f64p = C.POINTER(C.c_double)

@@ -13,7 +13,11 @@ from concurrent.futures import ThreadPoolExecutor
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
-LIB = os.path.join(HERE, "libsk_b200.so")
+# SK_VARIANT=name SK_DEFS="-DX=1 ..." builds an experiment variant libsk_b200_<name>.so
+VARIANT = os.environ.get("SK_VARIANT", "")
+EXTRA_DEFS = os.environ.get("SK_DEFS", "").split()
+LIB = os.path.join(HERE, f"libsk_b200_{VARIANT}.so" if VARIANT else "libsk_b200.so")
+OBJ_SUFFIX = f"_{VARIANT}" if VARIANT else ""
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ARCH + ["-lineinfo", "-O3", "--fmad=false", "-std=c++17", "-Xcompiler", "-fPIC",
@@ -28,7 +32,7 @@ def units():
     u.append(("sk_driver.cu", "sk_driver.o", []))
     u.append(("sk_problems.cpp", "sk_problems.o", []))
     u.append(("sk_comm.cpp", "sk_comm.o", []))
-    return u
+    return [(src, obj.replace(".o", OBJ_SUFFIX + ".o"), defs + EXTRA_DEFS) for src, obj, defs in u]
 
 
 def needs_build() -> bool:

@@ -19,6 +19,21 @@ constexpr int kSegsPerWarp = 4;            // aligned level-2 subtree per warp
 constexpr int kWarpsPerCta = 8;            // aligned level-5 subtree per CTA
 constexpr int kSegsPerCta = kSegsPerWarp * kWarpsPerCta;  // 32
 constexpr int kRowsPerCta = kSeg * kSegsPerCta;           // 16384
+// fused Lanczos / self-Gram kernels: one warp per segment, kFusedSegsPerCta
+// warps per CTA (an aligned subtree of the canonical tree)
+#ifndef SK_FUSED_SEGS
+#define SK_FUSED_SEGS 8
+#endif
+constexpr int kFusedSegsPerCta = SK_FUSED_SEGS;
+constexpr int kFusedThreads = 32 * kFusedSegsPerCta;
+#ifndef SK_P1_WARPS
+#define SK_P1_WARPS 32  // resident warps / SM for pass 1 (register budget 64)
+#endif
+#ifndef SK_P2_WARPS
+#define SK_P2_WARPS 48  // resident warps / SM for pass 2 (register budget 40)
+#endif
+constexpr int kP1Blocks = SK_P1_WARPS / kFusedSegsPerCta;
+constexpr int kP2Blocks = SK_P2_WARPS / kFusedSegsPerCta;
 constexpr int kTile = 32;                  // R2 core tile
 constexpr int kMaxS = 8;                   // device block-size limit
 constexpr double kPythGuard = 0x1p-10;

@@ -557,7 +557,7 @@ struct Solver {
     sk::SideConst& sc = c.side[sd];
     sc.row0 = pl.row0[P.rank];
     sc.dist = 1;
-    sc.chunk_f = pl.chunk_rows / (sk::kSeg * 8);  // kFusedSegsPerCta
+    sc.chunk_f = pl.chunk_rows / (sk::kSeg * sk::kFusedSegsPerCta);
     sc.chunk_g = pl.chunk_rows / sk::kRowsPerCta;
     sc.nch = pl.nch[P.rank];
     sc.halo = b.halo;

@@ -384,7 +384,6 @@ __device__ __forceinline__ void raw_row_csr(const SideConst& sc, const double* _
 // raw blocks, G_b = U_b^T x (R1), then c_b = N_b^{-T} G_b and M_b = N_b^{-1} c_b
 // are formed once per block; updates are x - sum_b U_b M_b.
 // =====================================================================
-constexpr int kFusedSegsPerCta = 8;
 enum UpdMode : int { UM_LANCZOS = 0, UM_FIRST = 1, UM_SECOND = 2, UM_CLEAN = 3, UM_INIT = 4 };
 
 template <int S>
@@ -523,7 +522,7 @@ __device__ __forceinline__ int row_mode(const SideConst& sc) {
 // K1: SpMM  w = (op U_{k-1}) N^{-1}   (sparse_matrix.cpp:142-158, order kept)
 // =====================================================================
 template <int S>
-__global__ void __launch_bounds__(256) k_spmm(SolveConst c) {
+__global__ void __launch_bounds__(256) k_spmm(const __grid_constant__ SolveConst c) {
   const int side = blockIdx.y;
   if (side >= c.nsides) return;
   const DevState* st = c.st;
@@ -561,48 +560,52 @@ __device__ __forceinline__ double tree32(double* a) {
   return a[0];
 }
 // Canonical tree over P CTA partials part[p*NE + e] for every e (last CTA):
-// aligned groups of 32 in registers, then the group nodes in smem.
+// levels of aligned groups of 32 (a tree over 32 = four aligned trees of 8),
+// intermediate nodes in global scratch (>= 2 * ceil(P/32) * NE doubles), the
+// last <= 32 nodes reduced per e. Aligned power-of-two groups compose, so this
+// is the canonical tree for any P.
 template <int NE>
-__device__ void final_tree(const double* part, int64_t P, double* out) {
-  constexpr int MAXG = NE <= 16 ? 128 : 32;  // static smem bound for large s
-  __shared__ double gnode[NE][MAXG];
-  const int64_t ngroups = (P + 31) / 32;
-  if (ngroups > MAXG) {
-    for (int e = threadIdx.x; e < NE; e += blockDim.x) out[e] = tree_stream(part + e, P, NE);
-    __syncthreads();
-    return;
-  }
-  for (int64_t idx = threadIdx.x; idx < NE * ngroups; idx += blockDim.x) {
-    const int e = (int)(idx % NE);
-    const int64_t grp = idx / NE;
-    const int64_t p0 = grp * 32;
-    const int cnt = (int)mn64(32, P - p0);
-    if (cnt == 32) {
-      // tree over 32 = tree over four aligned tree-of-8 nodes (same canonical tree)
-      double node[4];
+__device__ __noinline__ void final_tree(const double* part, int64_t P, double* out, double* scratch) {
+  const double* src = part;
+  int64_t cnt = P;
+  double* dst = scratch;
+  double* other = scratch + ((P + 31) / 32) * NE;
+  while (cnt > 32) {
+    const int64_t ngroups = (cnt + 31) / 32;
+    for (int64_t idx = threadIdx.x; idx < NE * ngroups; idx += blockDim.x) {
+      const int e = (int)(idx % NE);
+      const int64_t grp = idx / NE;
+      const int64_t p0 = grp * 32;
+      const int n32 = (int)mn64(32, cnt - p0);
+      double node;
+      if (n32 == 32) {
+        double q4[4];
 #pragma unroll 1
-      for (int q = 0; q < 4; ++q) {
-        double a[8];
+        for (int q = 0; q < 4; ++q) {
+          double a[8];
 #pragma unroll
-        for (int j = 0; j < 8; ++j) a[j] = __ldcg(part + (p0 + 8 * q + j) * NE + e);
+          for (int j = 0; j < 8; ++j) a[j] = __ldcg(src + (p0 + 8 * q + j) * NE + e);
 #pragma unroll
-        for (int w = 4; w >= 1; w >>= 1)
+          for (int w = 4; w >= 1; w >>= 1)
 #pragma unroll
-          for (int j = 0; j < w; ++j) a[j] = __dadd_rn(a[2 * j], a[2 * j + 1]);
-        node[q] = a[0];
+            for (int j = 0; j < w; ++j) a[j] = __dadd_rn(a[2 * j], a[2 * j + 1]);
+          q4[q] = a[0];
+        }
+        node = __dadd_rn(__dadd_rn(q4[0], q4[1]), __dadd_rn(q4[2], q4[3]));
+      } else {
+        node = tree_stream(src + p0 * NE + e, n32, NE);
       }
-      gnode[e][grp] = __dadd_rn(__dadd_rn(node[0], node[1]), __dadd_rn(node[2], node[3]));
-    } else {
-      gnode[e][grp] = tree_stream(part + p0 * NE + e, cnt, NE);
+      dst[grp * NE + e] = node;
     }
+    __threadfence_block();
+    __syncthreads();
+    src = dst;
+    cnt = ngroups;
+    double* t = dst;
+    dst = other;
+    other = t;
   }
-  __syncthreads();
-  for (int e = threadIdx.x; e < NE; e += blockDim.x) {
-    TreeStream ts;
-    ts.init();
-    for (int64_t grp = 0; grp < ngroups; ++grp) ts.push(gnode[e][grp]);
-    out[e] = ts.finish();
-  }
+  for (int e = threadIdx.x; e < NE; e += blockDim.x) out[e] = tree_stream(src + e, cnt, NE);
   __syncthreads();
 }
 template <int NE>
@@ -636,12 +639,12 @@ __device__ __forceinline__ int64_t node_off(const SolveConst& c, int64_t slot, i
   return ((slot * c.nsides + side) * c.nch_max + j) * c.nex;
 }
 template <int NE>
-__device__ void dist_emit(const SolveConst& c, int side, int64_t slot, const double* part, int64_t ncta,
-                          int64_t chunk) {
+__device__ __noinline__ void dist_emit(const SolveConst& c, int side, int64_t slot, const double* part, int64_t ncta,
+                          int64_t chunk, double* scratch) {
   const SideConst& sc = c.side[side];
   for (int64_t j = 0; j < sc.nch; ++j) {
     const int64_t p0 = j * chunk;
-    final_tree<NE>(part + p0 * NE, mn64(chunk, ncta - p0), c.nodes + node_off(c, slot, side, j));
+    final_tree<NE>(part + p0 * NE, mn64(chunk, ncta - p0), c.nodes + node_off(c, slot, side, j), scratch);
   }
 }
 // canonical tree over every rank's chunk nodes (all threads call; result in out)
@@ -711,7 +714,7 @@ __device__ inline bool gram_setup(const SolveConst& c, int side, int mode, const
 }
 
 template <int S>
-__global__ void __launch_bounds__(256) k_gram(SolveConst c, int mode) {
+__global__ void __launch_bounds__(256) k_gram(const __grid_constant__ SolveConst c, int mode) {
   constexpr int NB = S * S;
   const int side = blockIdx.z;
   if (side >= c.nsides) return;
@@ -829,7 +832,7 @@ __device__ __forceinline__ void p1_dispatch(const SideConst& sc, const double* _
 
 // pass-1 root -> c_b, M_b for blocks k-2 (if any) and k-1
 template <int S>
-__device__ void p1_finish(const SideConst& sc, int64_t k, const double* res) {
+__device__ __noinline__ void p1_finish(const SideConst& sc, int64_t k, const double* res) {
   constexpr int NB = S * S;
   if (threadIdx.x < 2) {
     const int slot = threadIdx.x;  // 0: block k-2, 1: block k-1
@@ -846,7 +849,7 @@ __device__ void p1_finish(const SideConst& sc, int64_t k, const double* res) {
 }
 // self-Gram root -> gbase (symmetric), then finalisation
 template <int S>
-__device__ void gram_finish(const SolveConst& c, int side, const double* res, int how) {
+__device__ __noinline__ void gram_finish(const SolveConst& c, int side, const double* res, int how) {
   constexpr int NS = S * (S + 1) / 2;
   SideState& sst = c.st->side[side];
   for (int e = threadIdx.x; e < NS; e += blockDim.x) {
@@ -870,11 +873,11 @@ __device__ void gram_finish(const SolveConst& c, int side, const double* res, in
 
 // Lanczos pass 1: w = (op U_{k-1}) N_{k-1}^{-1}; G = U_{k-2}^T w, U_{k-1}^T w
 // (block_krylov.cpp:71-84, CGS form). w is stored only for CSR operators.
-template <int S>
-__global__ void __launch_bounds__(256, 4) k_lanczos_p1(SolveConst c) {
+template <int S, int MODE>
+__global__ void __launch_bounds__(kFusedThreads, kP1Blocks) k_lanczos_p1(const __grid_constant__ SolveConst c, int side0) {
   constexpr int NB = S * S;
   constexpr int NE = 2 * NB;
-  const int side = blockIdx.z;
+  const int side = blockIdx.z + side0;
   if (side >= c.nsides) return;
   const DevState* st = c.st;
   if (st->status != RUNNING) return;
@@ -899,24 +902,15 @@ __global__ void __launch_bounds__(256, 4) k_lanczos_p1(SolveConst c) {
   double acc[NE];
 #pragma unroll
   for (int e = 0; e < NE; ++e) acc[e] = 0.0;
-  if (seg < nseg) {
-    const int64_t base = seg * kSeg;
-    switch (row_mode(sc)) {
-      case 2: p1_dispatch<S, 2>(sc, u1, f1, u0, two, base, sc.n, acc); break;
-      case 3: p1_dispatch<S, 3>(sc, u1, f1, u0, two, base, sc.n, acc); break;
-      case 12: p1_dispatch<S, 12>(sc, u1, f1, u0, two, base, sc.n, acc); break;
-      case 13: p1_dispatch<S, 13>(sc, u1, f1, u0, two, base, sc.n, acc); break;
-      default: p1_dispatch<S, 0>(sc, u1, f1, u0, two, base, sc.n, acc); break;
-    }
-  }
+  if (seg < nseg) p1_dispatch<S, MODE>(sc, u1, f1, u0, two, seg * kSeg, sc.n, acc);
   warp_seg_to_cta<NE>(acc, nvalid_cta, sc.part + cta * NE);
   if (!last_cta_arrive(sc.counter + 0, (unsigned)ncta)) return;
   if (sc.dist) {
-    dist_emit<NE>(c, side, 0, sc.part, ncta, sc.chunk_f);
+    dist_emit<NE>(c, side, 0, sc.part, ncta, sc.chunk_f, sc.part + ncta * NE);
     return;
   }
   __shared__ double res[NE];
-  final_tree<NE>(sc.part, ncta, res);
+  final_tree<NE>(sc.part, ncta, res, sc.part + ncta * NE);
   p1_finish<S>(sc, k, res);
 }
 
@@ -982,10 +976,10 @@ __device__ __forceinline__ void p2_dispatch(const SideConst& sc, const double* _
 
 // Lanczos pass 2: U_k = w - U_{k-2} M_{k-2} - U_{k-1} M_{k-1} (+ R1 self Gram,
 // finalise). Matrix-free operators recompute w from U_{k-1} instead of reading it.
-template <int S>
-__global__ void __launch_bounds__(256, 5) k_lanczos_p2(SolveConst c) {
+template <int S, int MODE>
+__global__ void __launch_bounds__(kFusedThreads, kP2Blocks) k_lanczos_p2(const __grid_constant__ SolveConst c, int side0) {
   constexpr int NS = S * (S + 1) / 2;
-  const int side = blockIdx.z;
+  const int side = blockIdx.z + side0;
   if (side >= c.nsides) return;
   const DevState* st = c.st;
   if (st->status != RUNNING) return;
@@ -1016,31 +1010,22 @@ __global__ void __launch_bounds__(256, 5) k_lanczos_p2(SolveConst c) {
   double acc[NS];
 #pragma unroll
   for (int e = 0; e < NS; ++e) acc[e] = 0.0;
-  if (seg < nseg) {
-    const int64_t base = seg * kSeg;
-    switch (row_mode(sc)) {
-      case 2: p2_dispatch<S, 2>(sc, u1, f1, u0, two, m1, m0, out, base, sc.n, acc); break;
-      case 3: p2_dispatch<S, 3>(sc, u1, f1, u0, two, m1, m0, out, base, sc.n, acc); break;
-      case 12: p2_dispatch<S, 12>(sc, u1, f1, u0, two, m1, m0, out, base, sc.n, acc); break;
-      case 13: p2_dispatch<S, 13>(sc, u1, f1, u0, two, m1, m0, out, base, sc.n, acc); break;
-      default: p2_dispatch<S, 0>(sc, u1, f1, u0, two, m1, m0, out, base, sc.n, acc); break;
-    }
-  }
+  if (seg < nseg) p2_dispatch<S, MODE>(sc, u1, f1, u0, two, m1, m0, out, seg * kSeg, sc.n, acc);
   warp_seg_to_cta<NS>(acc, nvalid_cta, sc.part + cta * NS);
   if (!last_cta_arrive(sc.counter + 1, (unsigned)ncta)) return;
   if (sc.dist) {
-    dist_emit<NS>(c, side, 0, sc.part, ncta, sc.chunk_f);
+    dist_emit<NS>(c, side, 0, sc.part, ncta, sc.chunk_f, sc.part + ncta * NS);
     return;
   }
   __shared__ double res[NS];
-  final_tree<NS>(sc.part, ncta, res);
+  final_tree<NS>(sc.part, ncta, res, sc.part + ncta * NS);
   gram_finish<S>(c, side, res, 0);
 }
 
 // Clean-up Gram (rare path): each CTA sweeps all blocks for its row group, so
 // the no-op launch stays one CTA per row group.
 template <int S>
-__global__ void __launch_bounds__(256) k_gram_loop(SolveConst c) {
+__global__ void __launch_bounds__(256) k_gram_loop(const __grid_constant__ SolveConst c) {
   constexpr int NB = S * S;
   const int side = blockIdx.z;
   if (side >= c.nsides) return;
@@ -1086,7 +1071,8 @@ __global__ void __launch_bounds__(256) k_gram_loop(SolveConst c) {
   }
   if (!last_cta_arrive(sc.counter + 2, (unsigned)sc.ncta)) return;
   if (sc.dist) {
-    for (int64_t b = 0; b < k; ++b) dist_emit<NB>(c, side, b, sc.part + b * sc.ncta * NB, sc.ncta, sc.chunk_g);
+    for (int64_t b = 0; b < k; ++b)
+      dist_emit<NB>(c, side, b, sc.part + b * sc.ncta * NB, sc.ncta, sc.chunk_g, sc.part + k * sc.ncta * NB);
     return;
   }
   for (int64_t b = threadIdx.x; b < k; b += blockDim.x) {
@@ -1111,7 +1097,7 @@ __device__ __forceinline__ const double* blk_ptr(const SideConst& sc, int64_t b)
   return reinterpret_cast<const double*>(__ldg(reinterpret_cast<const unsigned long long*>(sc.blocks) + b));
 }
 template <int S>
-__global__ void __launch_bounds__(kArnThreads) k_arn_update(SolveConst c, int mode) {
+__global__ void __launch_bounds__(kArnThreads) k_arn_update(const __grid_constant__ SolveConst c, int mode) {
   constexpr int UN = 8;
   constexpr int CH = (S <= 2 ? 1024 : 4096 / (S * S));  // M chunk (blocks), multiple of UN
   const int side = blockIdx.y;
@@ -1174,7 +1160,7 @@ __global__ void __launch_bounds__(kArnThreads) k_arn_update(SolveConst c, int mo
 
 // R1 self Gram x^T x of the candidate U_k (one warp per segment) + finalise.
 template <int S>
-__global__ void __launch_bounds__(256) k_self_gram(SolveConst c, int mode) {
+__global__ void __launch_bounds__(kFusedThreads) k_self_gram(const __grid_constant__ SolveConst c, int mode) {
   constexpr int NS = S * (S + 1) / 2;
   const int side = blockIdx.z;
   if (side >= c.nsides) return;
@@ -1216,7 +1202,7 @@ __global__ void __launch_bounds__(256) k_self_gram(SolveConst c, int mode) {
   warp_seg_to_cta<NS>(acc, nvalid_cta, sc.part + cta * NS);
   if (!last_cta_arrive(sc.counter + 1, (unsigned)ncta)) return;
   __shared__ double res[NS];
-  final_tree<NS>(sc.part, ncta, res);
+  final_tree<NS>(sc.part, ncta, res, sc.part + ncta * NS);
   SideState& sst = c.st->side[side];
   for (int e = threadIdx.x; e < NS; e += blockDim.x) {
     int t, u;
@@ -1242,7 +1228,7 @@ __global__ void __launch_bounds__(256) k_self_gram(SolveConst c, int mode) {
 // =====================================================================
 
 template <int S>
-__global__ void __launch_bounds__(256) k_update(SolveConst c, int mode) {
+__global__ void __launch_bounds__(256) k_update(const __grid_constant__ SolveConst c, int mode) {
   constexpr int NS = S * (S + 1) / 2;
   const int side = blockIdx.z;
   if (side >= c.nsides) return;
@@ -1343,7 +1329,7 @@ __global__ void __launch_bounds__(256) k_update(SolveConst c, int mode) {
   cta_combine<NS>(segv, g.nvalid_warp, g.nvalid_cta, sc.part + cta * NS);
   if (!last_cta_arrive(sc.counter + 1, (unsigned)sc.ncta)) return;
   if (sc.dist) {
-    dist_emit<NS>(c, side, 0, sc.part, sc.ncta, sc.chunk_g);
+    dist_emit<NS>(c, side, 0, sc.part, sc.ncta, sc.chunk_g, sc.part + sc.ncta * NS);
     return;
   }
   __shared__ double res[NS];
@@ -1468,7 +1454,7 @@ __device__ void householder_cta(double* W, double* Q, int64_t n, double* R, doub
 
 // which: 0 first-pass NEED_HH, 1 NEED_HH2 after clean-up, 2 init (U_0)
 template <int S>
-__global__ void __launch_bounds__(1024) k_householder(SolveConst c, int which) {
+__global__ void __launch_bounds__(1024) k_householder(const __grid_constant__ SolveConst c, int which) {
   const int side = blockIdx.x;
   if (side >= c.nsides) return;
   if (which != 2 && c.st->status != RUNNING) return;
@@ -1504,7 +1490,7 @@ __global__ void __launch_bounds__(1024) k_householder(SolveConst c, int which) {
 // Initialisation (block_krylov.cpp:27-52; factorized_solvers.cpp:121-131)
 // =====================================================================
 template <int S>
-__global__ void k_init_transpose(SolveConst c, const double* c1, const double* c2) {
+__global__ void k_init_transpose(const __grid_constant__ SolveConst c, const double* c1, const double* c2) {
   const int side = blockIdx.y;
   if (side >= c.nsides) return;
   const SideConst& sc = c.side[side];
@@ -1516,7 +1502,7 @@ __global__ void k_init_transpose(SolveConst c, const double* c1, const double* c
 }
 
 // R_0 = R_L R_R^T, P_0 = R_0, rho_0 = <R_0,R_0> (R2 contract, one tile)
-static __global__ void k_core_init(SolveConst c) {
+static __global__ void k_core_init(const __grid_constant__ SolveConst c) {
   DevState* st = c.st;
   const int s = c.s;
   if (threadIdx.x != 0) return;
@@ -1673,7 +1659,7 @@ __device__ inline bool any_side_broken(const SolveConst& c) {
 }
 
 template <int S>
-__global__ void __launch_bounds__(256) k_cg_a(SolveConst c) {
+__global__ void __launch_bounds__(256) k_cg_a(const __grid_constant__ SolveConst c) {
   DevState* st = c.st;
   if (st->status != RUNNING) return;
   if (any_side_broken(c)) {
@@ -1746,7 +1732,7 @@ __global__ void __launch_bounds__(256) k_cg_a(SolveConst c) {
 }
 
 template <int S>
-__global__ void __launch_bounds__(256) k_cg_b(SolveConst c) {
+__global__ void __launch_bounds__(256) k_cg_b(const __grid_constant__ SolveConst c) {
   DevState* st = c.st;
   if (st->status != RUNNING) return;
   const int64_t k = st->k;
@@ -1858,7 +1844,7 @@ __global__ void k_export_block(const double* blk, const double* nfac, int64_t b,
 // =====================================================================
 enum DistFin : int { DF_P1 = 0, DF_P2 = 1, DF_CGRAM = 2, DF_CSELF = 3 };
 template <int S>
-__global__ void __launch_bounds__(256) k_dist_fin(SolveConst c, int mode, int64_t msg) {
+__global__ void __launch_bounds__(256) k_dist_fin(const __grid_constant__ SolveConst c, int mode, int64_t msg) {
   constexpr int NB = S * S, NE = 2 * NB, NS = S * (S + 1) / 2;
   const int side = blockIdx.x;
   if (side >= c.nsides) return;
@@ -1902,7 +1888,7 @@ __global__ void __launch_bounds__(256) k_dist_fin(SolveConst c, int mode, int64_
 
 // newest block's first / last `halo` local rows -> hsend (lo | hi)
 template <int S>
-__global__ void k_halo_pack(SolveConst c) {
+__global__ void k_halo_pack(const __grid_constant__ SolveConst c) {
   const int side = blockIdx.y;
   if (side >= c.nsides) return;
   const SideConst& sc = c.side[side];
@@ -1917,7 +1903,7 @@ __global__ void k_halo_pack(SolveConst c) {
 }
 // hrecv (from previous | next rank) -> ghost rows of the newest block
 template <int S>
-__global__ void k_halo_unpack(SolveConst c) {
+__global__ void k_halo_unpack(const __grid_constant__ SolveConst c) {
   const int side = blockIdx.y;
   if (side >= c.nsides) return;
   const SideConst& sc = c.side[side];
@@ -1931,6 +1917,10 @@ __global__ void k_halo_unpack(SolveConst c) {
   }
 }
 
+static int host_row_mode(const SideConst& sc) {
+  if (sc.sdim == 0) return 0;
+  return sc.sdim + (sc.sg_pow2 >= 0 ? 10 : 0);
+}
 static int rows_grid(int64_t n) {
   int64_t g = (n + 255) / 256;
   if (g > 148 * 16) g = 148 * 16;
@@ -2013,19 +2003,42 @@ struct Launch {
     k_arn_update<S><<<dim3(g, c.nsides), kArnThreads, 0, st>>>(c, mode);
   }
   static void self_gram(const SolveConst& c, cudaStream_t st) {
-    k_self_gram<S><<<dim3(fused_grid(c), 1, c.nsides), 256, 0, st>>>(c, 0);
+    k_self_gram<S><<<dim3(fused_grid(c), 1, c.nsides), kFusedThreads, 0, st>>>(c, 0);
   }
   static unsigned fused_grid(const SolveConst& c) {
     int64_t m = 0;
     for (int s = 0; s < c.nsides; ++s) m = mx64(m, (c.side[s].nseg + kFusedSegsPerCta - 1) / kFusedSegsPerCta);
     return (unsigned)m;
   }
-  static void lanczos_p1(const SolveConst& c, cudaStream_t st) {
-    if constexpr (S <= 4) k_lanczos_p1<S><<<dim3(fused_grid(c), 1, c.nsides), 256, 0, st>>>(c);
+  template <int MODE>
+  static void fused_mode(const SolveConst& c, int pass, int side0, int nz, cudaStream_t st) {
+    if constexpr (S <= 4) {
+      if (pass == 1)
+        k_lanczos_p1<S, MODE><<<dim3(fused_grid(c), 1, nz), kFusedThreads, 0, st>>>(c, side0);
+      else
+        k_lanczos_p2<S, MODE><<<dim3(fused_grid(c), 1, nz), kFusedThreads, 0, st>>>(c, side0);
+    }
   }
-  static void lanczos_p2(const SolveConst& c, cudaStream_t st) {
-    if constexpr (S <= 4) k_lanczos_p2<S><<<dim3(fused_grid(c), 1, c.nsides), 256, 0, st>>>(c);
+  static void fused_side(const SolveConst& c, int pass, int mode, int side0, int nz, cudaStream_t st) {
+    switch (mode) {
+      case 2: fused_mode<2>(c, pass, side0, nz, st); break;
+      case 3: fused_mode<3>(c, pass, side0, nz, st); break;
+      case 12: fused_mode<12>(c, pass, side0, nz, st); break;
+      case 13: fused_mode<13>(c, pass, side0, nz, st); break;
+      default: fused_mode<0>(c, pass, side0, nz, st); break;
+    }
   }
+  static void fused(const SolveConst& c, int pass, cudaStream_t st) {
+    const int m0 = host_row_mode(c.side[0]);
+    if (c.nsides == 1 || host_row_mode(c.side[1]) == m0) {
+      fused_side(c, pass, m0, 0, c.nsides, st);
+    } else {
+      fused_side(c, pass, m0, 0, 1, st);
+      fused_side(c, pass, host_row_mode(c.side[1]), 1, 1, st);
+    }
+  }
+  static void lanczos_p1(const SolveConst& c, cudaStream_t st) { fused(c, 1, st); }
+  static void lanczos_p2(const SolveConst& c, cudaStream_t st) { fused(c, 2, st); }
   static void gram_loop(const SolveConst& c, cudaStream_t st) {
     int64_t nmax, cmax;
     dims(c, nmax, cmax);
@@ -2068,7 +2081,7 @@ __device__ __forceinline__ double hpacked(const double* hb, int64_t hld, int64_t
 // Leading structural zeros are skipped per tile; fma(0, x, acc) = acc for the
 // zero padding inside a tile (acc never -0, finite operands).
 constexpr int kImT = 64, kImK = 16;
-__global__ void __launch_bounds__(256) k_bi_image(SolveConst c, int which) {
+__global__ void __launch_bounds__(256) k_bi_image(const __grid_constant__ SolveConst c, int which) {
   DevState* st = c.st;
   if (st->status != RUNNING) return;
   const int s = c.s;
@@ -2158,7 +2171,7 @@ __global__ void __launch_bounds__(256) k_bi_image(SolveConst c, int which) {
 // H part (columns j < pc); part 1 adds the G part per the presence rule. The
 // fma chain of every output runs over l in ascending order (bitwise the above).
 constexpr int kBM = 128, kBK = 8;
-__global__ void __launch_bounds__(256, 1) k_bi_image2(SolveConst c, int which, int part) {
+__global__ void __launch_bounds__(256, 1) k_bi_image2(const __grid_constant__ SolveConst c, int which, int part) {
   DevState* st = c.st;
   if (st->status != RUNNING) return;
   const int s = c.s;
@@ -2284,7 +2297,7 @@ __device__ inline void bi_breakdown(const SolveConst& c) {
 }
 
 // after an extension pair: breakdown check and the image window (sched = (2k+2+which)s)
-__global__ void k_bi_begin(SolveConst c, int which) {
+__global__ void k_bi_begin(const __grid_constant__ SolveConst c, int which) {
   DevState* st = c.st;
   if (threadIdx.x != 0 || st->status != RUNNING) return;
   if (any_side_broken(c)) {
@@ -2316,7 +2329,7 @@ __device__ __forceinline__ double r2_small(const double* a, int64_t lda, const d
 }
 
 // denom = <R~0, Q>_{s x s}, guard on the angle, alpha (factorized_solvers.cpp:292-300)
-__global__ void k_bi_alpha(SolveConst c) {
+__global__ void k_bi_alpha(const __grid_constant__ SolveConst c) {
   DevState* st = c.st;
   if (st->status != RUNNING) return;
   const int s = c.s;
@@ -2335,7 +2348,7 @@ __global__ void k_bi_alpha(SolveConst c) {
 }
 
 // S = embed(R) - alpha Q over Q's window (factorized_solvers.cpp:301-302)
-__global__ void k_bi_s(SolveConst c) {
+__global__ void k_bi_s(const __grid_constant__ SolveConst c) {
   DevState* st = c.st;
   if (st->status != RUNNING) return;
   const int64_t rq = st->rows_q, cq = st->cols_q, rp = st->rows_p, cp = st->cols_p;
@@ -2351,7 +2364,7 @@ __global__ void k_bi_s(SolveConst c) {
 }
 
 // tt = <T,T>, ss = <S,S>, st = <S,T>_S (R2 over their windows), omega (:320-336)
-__global__ void __launch_bounds__(256) k_bi_omega(SolveConst c) {
+__global__ void __launch_bounds__(256) k_bi_omega(const __grid_constant__ SolveConst c) {
   DevState* st = c.st;
   if (st->status != RUNNING) return;
   const int64_t rt = st->rows_t, ct = st->cols_t, rs = st->rows_s, cs = st->cols_s;
@@ -2410,7 +2423,7 @@ __global__ void __launch_bounds__(256) k_bi_omega(SolveConst c) {
 
 // X = (embed(X) + alpha embed(P)) + omega S; R = embed(S) - omega T; ||R||; rho',
 // angle guard, beta (factorized_solvers.cpp:338-367)
-__global__ void __launch_bounds__(256) k_bi_update(SolveConst c) {
+__global__ void __launch_bounds__(256) k_bi_update(const __grid_constant__ SolveConst c) {
   DevState* st = c.st;
   if (st->status != RUNNING) return;
   const int64_t rt = st->rows_t, ct = st->cols_t, rs = st->rows_s, cs = st->cols_s;
@@ -2484,7 +2497,7 @@ __global__ void __launch_bounds__(256) k_bi_update(SolveConst c) {
 }
 
 // P = (R + beta embed(P)) + (-beta*omega) embed(Q) over R's window (:369-375)
-__global__ void k_bi_p(SolveConst c) {
+__global__ void k_bi_p(const __grid_constant__ SolveConst c) {
   DevState* st = c.st;
   if (st->status != RUNNING) return;
   const int64_t rt = st->rows_p, ct = st->cols_p, rp = st->rows_po, cp = st->cols_po;
@@ -2561,7 +2574,7 @@ void launch_rare(const SolveConst& c, int64_t kmax_blocks, cudaStream_t st) {
   SK_DISPATCH_S(c.s, householder(c, 1, st));
   g_launches += 4;
 }
-static __global__ void k_dist_pause(SolveConst c) {
+static __global__ void k_dist_pause(const __grid_constant__ SolveConst c) {
   DevState* st = c.st;
   if (threadIdx.x != 0 || st->status != RUNNING) return;
   for (int sd = 0; sd < c.nsides; ++sd) {
@@ -2569,7 +2582,7 @@ static __global__ void k_dist_pause(SolveConst c) {
     if (g == ST_NEED_HH || g == ST_NEED_CLEANUP) st->status = PAUSED;
   }
 }
-static __global__ void k_dist_resume(SolveConst c) {
+static __global__ void k_dist_resume(const __grid_constant__ SolveConst c) {
   if (threadIdx.x == 0 && c.st->status == PAUSED) c.st->status = RUNNING;
 }
 void launch_dist_fin(const SolveConst& c, int mode, int64_t msg, cudaStream_t st) {
