@@ -860,9 +860,22 @@ struct Solver {
     int64_t enq = 0, checked = 0;
     bool done = false;
     const bool fused = sk::lanczos_fused_ok(c) && !getenv("SK_NO_FUSED");
+    // CG: the rare paths (Householder / clean-up) run only when an extension
+    // asks for them: pass 2 ends with a pause check, the host sees PAUSED in the
+    // status ring, drains the (no-op) run-ahead and runs them for that iteration.
+    const bool pause_mode = !arnoldi && !cfg.capture_iterates && !getenv("SK_NO_PAUSE");
+    auto cg_cores = [&](int64_t k) {
+      const double rp = (double)((k + 1) * s), rq = (double)((k + 2) * s);
+      timed(4, 8.0 * 3 * rp * rp, [&] { sk::launch_cg_a(c, (k + 1) * s, st); });
+      dbg("core_a", k);
+      timed(5, 8.0 * (4 * rp * rp + rq * rq), [&] { sk::launch_cg_b(c, (k + 2) * s, st); });
+      dbg("core_b", k);
+    };
     std::vector<std::vector<double>> caps;
     std::vector<std::pair<int64_t, int64_t>> cap_shape;
-    for (int64_t k = 0; k < max_iter && !done; ++k) {
+    int64_t k_start = 0;
+  restart:
+    for (int64_t k = k_start; k < max_iter && !done; ++k) {
       if (arnoldi) {
         for (int sd = 0; sd < nsides; ++sd) ensure_blocks(sd, 2 * k + 3);
         ensure_hcap(2 * k + 2);
@@ -893,12 +906,15 @@ struct Solver {
         timed(3, pass_bytes(k, 2), [&] { sk::launch_lanczos_update(c, k + 1, st); });
         dbg("update", k);
       }
-      timed(2, 0.0, [&] { sk::launch_rare(c, k + 1, st); });
+      if (pause_mode) {
+        sk::launch_dist_pause(c, st);
+      } else {
+        timed(2, 0.0, [&] { sk::launch_rare(c, k + 1, st); });
+      }
       dbg("rare", k);
-      timed(4, 8.0 * 3 * rp * rp, [&] { sk::launch_cg_a(c, (k + 1) * s, st); });
-      dbg("core_a", k);
-      timed(5, 8.0 * (4 * rp * rp + rq * rq), [&] { sk::launch_cg_b(c, (k + 2) * s, st); });
-      dbg("core_b", k);
+      (void)rp;
+      (void)rq;
+      cg_cores(k);
       }
       CK(cudaMemcpyAsync(&hstat[k % RING], &dstate->status, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
       CK(cudaEventRecord(rev[k % RING], st));
@@ -929,6 +945,19 @@ struct Solver {
           break;
         }
         CK(q);
+        if (hstat[checked % RING] == sk::PAUSED) {
+          const int64_t kp = read_state().k;  // later iterations were no-ops
+          sk::launch_dist_resume(c, st);
+          timed(2, 0.0, [&] { sk::launch_rare(c, kp + 1, st); });
+          dbg("rare", kp);
+          cg_cores(kp);
+          CK(cudaMemcpyAsync(&hstat[kp % RING], &dstate->status, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+          CK(cudaEventRecord(rev[kp % RING], st));
+          enq = kp + 1;
+          checked = kp;
+          k = kp;  // the loop continues at kp + 1
+          continue;
+        }
         if (hstat[checked % RING] != sk::RUNNING) {
           done = true;
           break;
@@ -936,6 +965,20 @@ struct Solver {
         ++checked;
       }
       if (P.profile) drain_events(false);
+    }
+    if (pause_mode && !done) {
+      // a pause among the last enqueued iterations: finish it, then resume
+      const sk::DevState hs = read_state();
+      if (hs.status == sk::PAUSED) {
+        sk::launch_dist_resume(c, st);
+        timed(2, 0.0, [&] { sk::launch_rare(c, hs.k + 1, st); });
+        cg_cores(hs.k);
+        if (read_state().status == sk::RUNNING && hs.k + 1 < max_iter) {
+          k_start = hs.k + 1;
+          enq = checked = k_start;
+          goto restart;
+        }
+      }
     }
     CK(cudaEventRecord(t1, st));
     CK(cudaStreamSynchronize(st));
