@@ -740,7 +740,7 @@ struct Solver {
     dfree(ccounter);
     const int64_t nt = ncap / 32;
     cpart = dalloc<double>(3 * nt * nt + nt + 1024);
-    ccounter = dalloc<unsigned int>(8);
+    ccounter = dalloc<unsigned int>(nt + 16);  // 0..7 global, 8.. per tile column (R2 reductions)
     rcap = ncap;
     c.X = X;
     c.R = R;

@@ -1636,17 +1636,59 @@ __device__ __forceinline__ double tile_reduce(const double* f, int nrows, int nc
   return butterfly(acc);
 }
 
+// Canonical pairwise tree over the cnt (<= 32) values held by lanes 0..cnt-1:
+// strides 1, 2, 4, ..., a node without a right child passes through.
+__device__ __forceinline__ double warp_tree(double v, int cnt) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const double o = __shfl_down_sync(0xffffffffu, v, d);
+    if ((lane & (2 * d - 1)) == 0 && lane + d < cnt) v = __dadd_rn(v, o);
+  }
+  return __shfl_sync(0xffffffffu, v, 0);
+}
+// canonical tree over a[0..n) (stride st) by one warp: aligned groups of 32,
+// then the group nodes. GLOBAL: a[] was written by other CTAs (L2 loads);
+// otherwise a[] may be shared memory (generic loads).
+template <bool GLOBAL>
+static __device__ double warp_tree_n(const double* a, int64_t n, int64_t st) {
+  const int lane = threadIdx.x & 31;
+  auto ld = [&](int64_t i) { return GLOBAL ? __ldcg(a + i * st) : a[i * st]; };
+  if (n <= 32) return warp_tree(lane < n ? ld(lane) : 0.0, (int)n);
+  const int64_t ng = (n + 31) / 32;
+  if (ng <= 32) {
+    double node = 0.0;
+    for (int64_t g = 0; g < ng; ++g) {
+      const int64_t idx = g * 32 + lane;
+      const double t = warp_tree(idx < n ? ld(idx) : 0.0, (int)mn64(32, n - g * 32));
+      if (lane == g) node = t;
+    }
+    return warp_tree(node, (int)ng);
+  }
+  // > 1024 values (not reached for core tiles, r <= 32768): one lane streams
+  double v = 0.0;
+  if (lane == 0) {
+    TreeStream ts;
+    ts.init();
+    for (int64_t i = 0; i < n; ++i) ts.push(ld(i));
+    v = ts.finish();
+  }
+  return __shfl_sync(0xffffffffu, v, 0);
+}
+// R2 root: per tile column a canonical tree over its row tiles, then over the
+// columns (one warp per column, then one warp over the column nodes)
 static __device__ double r2_final(const double* part, int64_t nti, int64_t ntj, double* scratch) {
-  for (int64_t tj = threadIdx.x; tj < ntj; tj += blockDim.x)
-    scratch[tj] = tree_stream(part + tj * nti, nti, 1);
+  const int warp = threadIdx.x >> 5, nw = blockDim.x >> 5, lane = threadIdx.x & 31;
+  for (int64_t tj = warp; tj < ntj; tj += nw) {
+    const double v = warp_tree_n<true>(part + tj * nti, nti, 1);
+    if (lane == 0) scratch[tj] = v;
+  }
   __threadfence_block();
   __syncthreads();
   __shared__ double res;
-  if (threadIdx.x == 0) {
-    TreeStream ts;
-    ts.init();
-    for (int64_t tj = 0; tj < ntj; ++tj) ts.push(scratch[tj]);
-    res = ts.finish();
+  if (warp == 0) {
+    const double v = warp_tree_n<false>(scratch, ntj, 1);
+    if (lane == 0) res = v;
   }
   __syncthreads();
   return res;
@@ -1656,6 +1698,132 @@ __device__ inline bool any_side_broken(const SolveConst& c) {
   for (int s = 0; s < c.nsides; ++s)
     if (c.st->side[s].broken) return true;
   return false;
+}
+
+// ---- CG core tiles (K4) ----
+// A CTA owns one 32x32 tile of the core. It stages P with a halo of 2S rows /
+// columns, the H-band coefficients of its 32 rows and the G-band coefficients
+// of its 32 columns in shared memory (32-bit tile-local indexing), then every
+// entry forms image(P)(i,j) = sum_jb [sum_t H(i,l) P(l,j)] + sum_jb [sum_t P(i,l)
+// G(j,l)] in exactly image_at's order (jb ascending, t ascending, one partial
+// per band block).
+template <int S>
+struct CoreSmem {
+  static constexpr int H = CgTile<S>::H, D = CgTile<S>::D;
+  double sp[D * D];
+  double hc[3 * S][kTile];  // H(i0+li, (bi-1)S + q)
+  double gc[3 * S][kTile];  // G(j0+lj, (bj-1)S + q)
+  // tile products f (kTile^2) reuse sp once every entry is formed
+  int hlo[kTile], hhi[kTile], glo[kTile], ghi[kTile];  // valid band blocks (absolute)
+};
+template <int S>
+__device__ void stage_bands(CoreSmem<S>& sm, const double* hv, const double* hw, int i0, int j0, int pr,
+                            int pc) {
+  const int JBr = pr / S, JBc = pc / S;
+  for (int idx = threadIdx.x; idx < 3 * S * kTile; idx += blockDim.x) {
+    const int q = idx / kTile, li = idx % kTile;
+    {
+      const int i = i0 + li, bi = i / S;
+      const int lo = bi - 1 > 0 ? bi - 1 : 0, hi = bi + 1 < JBr - 1 ? bi + 1 : JBr - 1;
+      const int jb = bi - 1 + q / S;
+      sm.hc[q][li] = (jb >= lo && jb <= hi) ? band_at(hv, S, i, (int64_t)jb * S + q % S) : 0.0;
+      if (q == 0) {
+        sm.hlo[li] = lo;
+        sm.hhi[li] = hi;
+      }
+    }
+    {
+      const int j = j0 + li, bj = j / S;
+      const int lo = bj - 1 > 0 ? bj - 1 : 0, hi = bj + 1 < JBc - 1 ? bj + 1 : JBc - 1;
+      const int jb = bj - 1 + q / S;
+      sm.gc[q][li] = (jb >= lo && jb <= hi) ? band_at(hw, S, j, (int64_t)jb * S + q % S) : 0.0;
+      if (q == 0) {
+        sm.glo[li] = lo;
+        sm.ghi[li] = hi;
+      }
+    }
+  }
+}
+// image(P) at tile-local (li, lj); i = i0 + li < rows of the window, j = j0 + lj
+template <int S>
+__device__ __forceinline__ double core_image(const CoreSmem<S>& sm, int li, int lj, int i0, int j0, int pr, int pc) {
+  constexpr int H = CgTile<S>::H, D = CgTile<S>::D;
+  const int i = i0 + li, j = j0 + lj;
+  const bool hasH = j < pc, hasG = i < pr;
+  double hpart = 0.0, gpart = 0.0;
+  if (hasH) {
+    const int bi = i / S, lo = sm.hlo[li], hi = sm.hhi[li];
+    const double* pcol = sm.sp + (lj + H) * D + H - i0;  // pcol[l] = P(l, j)
+#pragma unroll
+    for (int qb = 0; qb < 3; ++qb) {
+      const int jb = bi - 1 + qb;
+      if (jb >= lo && jb <= hi) {
+        double d = 0.0;
+#pragma unroll
+        for (int t = 0; t < S; ++t) d = __dadd_rn(d, __dmul_rn(sm.hc[qb * S + t][li], pcol[jb * S + t]));
+        hpart = __dadd_rn(hpart, d);
+      }
+    }
+  }
+  if (hasG) {
+    const int bj = j / S, lo = sm.glo[lj], hi = sm.ghi[lj];
+    const double* prow = sm.sp + (li + H) + (H - j0) * D;  // prow[l * D] = P(i, l)
+#pragma unroll
+    for (int qb = 0; qb < 3; ++qb) {
+      const int jb = bj - 1 + qb;
+      if (jb >= lo && jb <= hi) {
+        double d = 0.0;
+#pragma unroll
+        for (int t = 0; t < S; ++t) d = __dadd_rn(d, __dmul_rn(prow[(jb * S + t) * D], sm.gc[qb * S + t][lj]));
+        gpart = __dadd_rn(gpart, d);
+      }
+    }
+  }
+  if (hasH && hasG) return __dadd_rn(hpart, gpart);
+  return hasH ? hpart : (hasG ? gpart : 0.0);
+}
+template <int S>
+__device__ void stage_p32(CoreSmem<S>& sm, const SolveConst& c, int i0, int j0, int rows_p, int cols_p, int mode,
+                          const double* Pprev, const double* Pcur, double beta, bool first) {
+  constexpr int H = CgTile<S>::H, D = CgTile<S>::D;
+  const int64_t ld = c.ld;
+  for (int idx = threadIdx.x; idx < D * D; idx += blockDim.x) {
+    const int li = idx % D, lj = idx / D;
+    const int i = i0 - H + li, j = j0 - H + lj;
+    double v = 0.0;
+    if (i >= 0 && j >= 0 && i < rows_p && j < cols_p) {
+      const int64_t o = (int64_t)j * ld + i;
+      if (mode == 1)
+        v = Pcur[o];
+      else if (first)
+        v = c.R[o];
+      else
+        v = __dadd_rn(c.R[o], __dmul_rn(beta, Pprev[o]));
+    }
+    sm.sp[idx] = v;
+  }
+}
+// R2 root with the reduction spread over the tile columns: the last CTA of a
+// column reduces that column's tile partials (canonical tree over tile rows),
+// the last column to finish reduces the column nodes. True in exactly one CTA.
+static __device__ bool r2_columns(const SolveConst& c, int64_t nti, int64_t ntj, int64_t tj, double* root) {
+  unsigned int* colctr = c.ccounter + 8;
+  double* colnode = c.cpart + nti * ntj;
+  if (!last_cta_arrive(colctr + tj, (unsigned)nti)) return false;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (warp == 0) {
+    const double v = warp_tree_n<true>(c.cpart + tj * nti, nti, 1);
+    if (lane == 0) colnode[tj] = v;
+  }
+  if (!last_cta_arrive(c.ccounter + 0, (unsigned)ntj)) return false;
+  __shared__ double res;
+  if (warp == 0) {
+    const double v = warp_tree_n<true>(colnode, ntj, 1);
+    if (lane == 0) res = v;
+  }
+  __syncthreads();
+  *root = res;
+  return true;
 }
 
 template <int S>
@@ -1673,46 +1841,49 @@ __global__ void __launch_bounds__(256) k_cg_a(const __grid_constant__ SolveConst
     return;
   }
   const int64_t k = st->k;
-  const int64_t rows_p = st->rows_p, cols_p = st->cols_p;
+  const int rows_p = (int)st->rows_p, cols_p = (int)st->cols_p;
   const int64_t nti = (rows_p + kTile - 1) / kTile, ntj = (cols_p + kTile - 1) / kTile;
   const int64_t ti = blockIdx.x, tj = blockIdx.y;
   if (ti >= nti || tj >= ntj) return;
   if (ti == 0 && tj == 0 && threadIdx.x == 0) c.hist_tk[k + 1] = (double)globaltimer();
-  constexpr int D = CgTile<S>::D;
-  __shared__ double sp[D * D];
-  __shared__ double f[kTile * kTile];
-  const int64_t i0 = ti * kTile, j0 = tj * kTile;
+  constexpr int H = CgTile<S>::H, D = CgTile<S>::D;
+  __shared__ CoreSmem<S> sm;
+  const int i0 = (int)ti * kTile, j0 = (int)tj * kTile;
   const double* Pprev = c.P[(k + 1) & 1];
   double* Pnew = c.P[k & 1];
-  stage_p<S>(sp, c, i0, j0, rows_p, cols_p, 0, Pprev, nullptr, st->beta, k == 0);
-  __syncthreads();
   const SideConst& sv = c.side[0];
   const SideConst& sw = c.side[c.nsides > 1 ? 1 : 0];
+  stage_p32<S>(sm, c, i0, j0, rows_p, cols_p, 0, Pprev, nullptr, st->beta, k == 0);
+  stage_bands<S>(sm, sv.hband, sw.hband, i0, j0, rows_p, cols_p);
+  __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int64_t i = i0 + lane;
+  const int i = i0 + lane;
+  const int64_t ld = c.ld;
+  double fv[4];
+#pragma unroll
   for (int q = 0; q < 4; ++q) {
     const int lc = warp * 4 + q;
-    const int64_t j = j0 + lc;
-    double fv = 0.0;
+    const int j = j0 + lc;
+    fv[q] = 0.0;
     if (i < rows_p && j < cols_p) {
-      constexpr int H = CgTile<S>::H;
-      const double pv = sp[(lc + H) * D + (lane + H)];
-      Pnew[j * c.ld + i] = pv;
-      const double qv = image_at<S>(sp, sv.hband, sw.hband, i, j, i0, j0, rows_p, cols_p);
-      fv = __dmul_rn(c.R[j * c.ld + i], qv);
+      const double pv = sm.sp[(lc + H) * D + (lane + H)];
+      Pnew[(int64_t)j * ld + i] = pv;
+      const double qv = core_image<S>(sm, lane, lc, i0, j0, rows_p, cols_p);
+      fv[q] = __dmul_rn(c.R[(int64_t)j * ld + i], qv);
     }
-    f[lc * kTile + lane] = fv;
   }
+  __syncthreads();
+  double* f = sm.sp;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) f[(warp * 4 + q) * kTile + lane] = fv[q];
   __syncthreads();
   if (warp == 0) {
     const int nr = (int)mn64(kTile, rows_p - i0), nc = (int)mn64(kTile, cols_p - j0);
     const double v = tile_reduce(f, nr, nc);
     if (lane == 0) c.cpart[tj * nti + ti] = v;
   }
-  if (!last_cta_arrive(c.ccounter, (unsigned)(nti * ntj))) return;
-  __shared__ double scratch[256];
-  double* scr = ntj <= 256 ? scratch : c.cpart + nti * ntj;
-  const double denom = r2_final(c.cpart, nti, ntj, scr);
+  double denom;
+  if (!r2_columns(c, nti, ntj, tj, &denom)) return;
   if (threadIdx.x == 0) {
     st->denom = denom;
     if (fabs(denom) < __dmul_rn(c.tol, st->rho)) {  // factorized_solvers.cpp:155-160
@@ -1736,52 +1907,56 @@ __global__ void __launch_bounds__(256) k_cg_b(const __grid_constant__ SolveConst
   DevState* st = c.st;
   if (st->status != RUNNING) return;
   const int64_t k = st->k;
-  const int64_t rows_p = st->rows_p, cols_p = st->cols_p;
-  const int64_t rows_q = st->rows_q, cols_q = st->cols_q;
+  const int rows_p = (int)st->rows_p, cols_p = (int)st->cols_p;
+  const int rows_q = (int)st->rows_q, cols_q = (int)st->cols_q;
   const int64_t nti = (rows_q + kTile - 1) / kTile, ntj = (cols_q + kTile - 1) / kTile;
   const int64_t ti = blockIdx.x, tj = blockIdx.y;
   if (ti >= nti || tj >= ntj) return;
   constexpr int D = CgTile<S>::D, H = CgTile<S>::H;
-  __shared__ double sp[D * D];
-  __shared__ double f[kTile * kTile];
-  const int64_t i0 = ti * kTile, j0 = tj * kTile;
+  __shared__ CoreSmem<S> sm;
+  const int i0 = (int)ti * kTile, j0 = (int)tj * kTile;
   const double* Pcur = c.P[k & 1];
-  stage_p<S>(sp, c, i0, j0, rows_p, cols_p, 1, nullptr, Pcur, 0.0, false);
-  __syncthreads();
   const SideConst& sv = c.side[0];
   const SideConst& sw = c.side[c.nsides > 1 ? 1 : 0];
+  stage_p32<S>(sm, c, i0, j0, rows_p, cols_p, 1, nullptr, Pcur, 0.0, false);
+  stage_bands<S>(sm, sv.hband, sw.hband, i0, j0, rows_p, cols_p);
+  __syncthreads();
   const double alpha = st->alpha, nalpha = -alpha;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int64_t i = i0 + lane;
+  const int i = i0 + lane;
+  const int64_t ld = c.ld;
+  double fv[4];
+#pragma unroll
   for (int q = 0; q < 4; ++q) {
     const int lc = warp * 4 + q;
-    const int64_t j = j0 + lc;
-    double fv = 0.0;
+    const int j = j0 + lc;
+    fv[q] = 0.0;
     if (i < rows_q && j < cols_q) {
-      const double qv = image_at<S>(sp, sv.hband, sw.hband, i, j, i0, j0, rows_p, cols_p);
-      const int64_t o = j * c.ld + i;
+      const double qv = core_image<S>(sm, lane, lc, i0, j0, rows_p, cols_p);
+      const int64_t o = (int64_t)j * ld + i;
       const bool inp = i < rows_p && j < cols_p;
       const double remb = inp ? c.R[o] : 0.0;
       const double rn = __dadd_rn(remb, __dmul_rn(nalpha, qv));
       c.R[o] = rn;
-      fv = __dmul_rn(rn, rn);
+      fv[q] = __dmul_rn(rn, rn);
       if (inp) {
-        const double pv = sp[(lc + H) * D + (lane + H)];
+        const double pv = sm.sp[(lc + H) * D + (lane + H)];
         c.X[o] = __dadd_rn(c.X[o], __dmul_rn(alpha, pv));
       }
     }
-    f[lc * kTile + lane] = fv;
   }
+  __syncthreads();
+  double* f = sm.sp;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) f[(warp * 4 + q) * kTile + lane] = fv[q];
   __syncthreads();
   if (warp == 0) {
     const int nr = (int)mn64(kTile, rows_q - i0), nc = (int)mn64(kTile, cols_q - j0);
     const double v = tile_reduce(f, nr, nc);
     if (lane == 0) c.cpart[tj * nti + ti] = v;
   }
-  if (!last_cta_arrive(c.ccounter, (unsigned)(nti * ntj))) return;
-  __shared__ double scratch[256];
-  double* scr = ntj <= 256 ? scratch : c.cpart + nti * ntj;
-  const double rho_next = r2_final(c.cpart, nti, ntj, scr);
+  double rho_next;
+  if (!r2_columns(c, nti, ntj, tj, &rho_next)) return;
   if (threadIdx.x == 0) {
     const double norm_r = __dsqrt_rn(rho_next);
     const double rel = __ddiv_rn(norm_r, st->norm_r0);
