@@ -116,6 +116,27 @@ def test_history_within_reference_order_tolerance(sk, po):
     assert max_rel(h[:21], ref.rel_residual[:21]) <= 1e-10
 
 
+def test_config1_x_parity_and_iterations_vs_reference_order(sk, po):
+    """North-star parity against the reference-order restatement (the reference's
+    own loop orders) on BASELINE config 1: history within 1e-10 relative, the same
+    iteration count (+-1), and ||X_gpu - X_ref||_F / ||X_ref||_F <= 1e-8 with X formed
+    densely (n = 4096), so no Gram-product cancellation enters the metric."""
+    a = po.laplacian_2d(64)
+    c1 = po.random_rhs(4096, 1, 1234)
+    c1 /= np.linalg.norm(c1)
+    c2 = po.random_rhs(4096, 1, 1235)
+    c2 /= np.linalg.norm(c2)
+    ref = po.factorized_cg(a, a, c1, c2, po.Config(eps_tol=1e-8, max_iter=500), po.REFERENCE_ORDER)
+    sol = sk.factorized_cg(to_sk(sk, a), to_sk(sk, a), c1, c2, _cfg(sk, eps_tol=1e-8, max_iter=500))
+    h = sol.history.rel_residuals()
+    assert abs(h.size - ref.rel_residual.size) <= 1
+    m = min(h.size, ref.rel_residual.size)
+    assert max_rel(h[:m], ref.rel_residual[:m]) <= 1e-10
+    x_gpu = sol.V @ sol.core @ sol.W.T
+    x_ref = ref.V @ ref.core @ ref.W.T
+    assert np.linalg.norm(x_gpu - x_ref) <= 1e-8 * np.linalg.norm(x_ref)
+
+
 @pytest.mark.parametrize("env", ["SK_NO_STENCIL", "SK_NO_FUSED"])
 def test_kernel_variants_bitwise(sk, po, env, monkeypatch):
     """Matrix-free stencil vs CSR gather, fused vs generic Lanczos passes: identical bits."""
