@@ -326,7 +326,7 @@ def main():
         line["e2e"] = {"value": e2e_its / e2e_s, "unit": UNIT,
                        "h2d_bytes_per_step": h2d // args.e2e_steps,
                        "d2h_bytes_per_step": d2h // args.e2e_steps,
-                       "note": "includes host CSR validation/symmetry checks/transposition"}
+                       "note": "includes host CSR validation, symmetry check, stencil detection (all host threads) and the H2D of C1, C2"}
 
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:

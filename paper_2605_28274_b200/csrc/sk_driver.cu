@@ -19,6 +19,9 @@
 #include <memory>
 #include <stdexcept>
 #include <string>
+#include <thread>
+#include <mutex>
+#include <atomic>
 #include <vector>
 
 namespace {
@@ -48,22 +51,97 @@ struct HostCsr {
   std::vector<double> val;
 };
 
+// Host row loops run on all host threads (the e2e path validates and inspects
+// CSRs of up to 84M entries per call). f(lo, hi) gets a contiguous row range.
+int host_threads() {
+  static const int t = [] {
+    int h = (int)std::thread::hardware_concurrency();
+    if (const char* e = getenv("SK_HOST_THREADS")) h = std::atoi(e);
+    return std::max(1, std::min(h, 64));
+  }();
+  return t;
+}
+template <class F>
+void par_rows(int64_t n, F&& f) {
+  const int T = (int)std::min<int64_t>(host_threads(), std::max<int64_t>(1, n / 65536));
+  if (T <= 1) {
+    f(int64_t(0), n);
+    return;
+  }
+  std::vector<std::thread> th;
+  th.reserve(T);
+  for (int t = 0; t < T; ++t) th.emplace_back([&, t] { f(n * t / T, n * (t + 1) / T); });
+  for (auto& x : th) x.join();
+}
+
+// SparseMatrix invariants (sparse_matrix.cpp:12-32). Rows are checked in
+// parallel; the reported error is the one of the lowest offending row, as a
+// sequential scan would report.
 void validate_csr(const sk_csr* a, const char* what) {
   if (!a || !a->row_ptr || (a->nnz > 0 && (!a->col_idx || !a->values)))
     throw SkError(SK_ERR_INVALID_MATRIX, std::string(what) + ": null CSR");
   if (a->n_rows < 0 || a->n_cols < 0) throw SkError(SK_ERR_INVALID_MATRIX, "SparseMatrix: negative dimension");
   if (a->row_ptr[0] != 0 || a->row_ptr[a->n_rows] != a->nnz)
     throw SkError(SK_ERR_INVALID_MATRIX, "SparseMatrix: row_ptr endpoints inconsistent with nnz");
-  for (int64_t i = 0; i < a->n_rows; ++i) {
-    if (a->row_ptr[i] > a->row_ptr[i + 1])
-      throw SkError(SK_ERR_INVALID_MATRIX, "SparseMatrix: row_ptr not nondecreasing");
-    for (int64_t k = a->row_ptr[i]; k < a->row_ptr[i + 1]; ++k) {
-      if (a->col_idx[k] < 0 || a->col_idx[k] >= a->n_cols)
-        throw SkError(SK_ERR_INVALID_MATRIX, "SparseMatrix: column index out of range");
-      if (k > a->row_ptr[i] && a->col_idx[k] <= a->col_idx[k - 1])
-        throw SkError(SK_ERR_INVALID_MATRIX, "SparseMatrix: column indices not strictly increasing in row");
+  std::mutex mu;
+  int64_t bad_row = INT64_MAX;
+  int bad_kind = 0;
+  par_rows(a->n_rows, [&](int64_t lo, int64_t hi) {
+    for (int64_t i = lo; i < hi; ++i) {
+      int kind = 0;
+      const int64_t k0 = a->row_ptr[i], k1 = a->row_ptr[i + 1];
+      if (k0 > k1) {
+        kind = 1;
+      } else {
+        for (int64_t k = k0; k < k1; ++k) {
+          if (a->col_idx[k] < 0 || a->col_idx[k] >= a->n_cols) {
+            kind = 2;
+            break;
+          }
+          if (k > k0 && a->col_idx[k] <= a->col_idx[k - 1]) {
+            kind = 3;
+            break;
+          }
+        }
+      }
+      if (kind) {
+        std::lock_guard<std::mutex> g(mu);
+        if (i < bad_row) {
+          bad_row = i;
+          bad_kind = kind;
+        }
+        return;
+      }
     }
-  }
+  });
+  if (bad_kind == 1) throw SkError(SK_ERR_INVALID_MATRIX, "SparseMatrix: row_ptr not nondecreasing");
+  if (bad_kind == 2) throw SkError(SK_ERR_INVALID_MATRIX, "SparseMatrix: column index out of range");
+  if (bad_kind == 3)
+    throw SkError(SK_ERR_INVALID_MATRIX, "SparseMatrix: column indices not strictly increasing in row");
+}
+
+// A == A^T bitwise (same pattern, bit-identical mirrored values). For a valid
+// CSR (strictly increasing columns) this means transposed() (sparse_matrix.cpp:
+// 80-95) returns A's own arrays, and ||A - A^T||_F = 0 (:109-132). Each entry
+// finds its mirror by binary search; no transpose is formed.
+bool bitwise_symmetric(const sk_csr* a) {
+  if (a->n_rows != a->n_cols) return false;
+  std::atomic<bool> ok{true};
+  par_rows(a->n_rows, [&](int64_t lo, int64_t hi) {
+    for (int64_t i = lo; i < hi && ok.load(std::memory_order_relaxed); ++i)
+      for (int64_t k = a->row_ptr[i]; k < a->row_ptr[i + 1]; ++k) {
+        const int64_t j = a->col_idx[k];
+        if (j == i) continue;
+        const int64_t* b = a->col_idx + a->row_ptr[j];
+        const int64_t* e = a->col_idx + a->row_ptr[j + 1];
+        const int64_t* p = std::lower_bound(b, e, i);
+        if (p == e || *p != i || std::memcmp(&a->values[p - a->col_idx], &a->values[k], sizeof(double)) != 0) {
+          ok.store(false, std::memory_order_relaxed);
+          return;
+        }
+      }
+  });
+  return ok.load();
 }
 
 HostCsr transpose(const sk_csr* a) {
@@ -157,8 +235,8 @@ bool detect_stencil(const int64_t* rp, const int64_t* ci, const double* val, int
     }
     bool have[7] = {false, false, false, false, false, false, false};
     double cval[7] = {0, 0, 0, 0, 0, 0, 0};
-    bool ok = true;
-    for (int64_t i = 0; i < n && ok; ++i) {
+    // row i matches the stencil; learn = adopt a slot's first value seen
+    auto row_ok = [&](int64_t i, bool learn) {
       const int64_t ix = i % g, iy = (i / g) % g, iz = i / g2;
       bool present[7];
       if (dim == 2) {
@@ -169,24 +247,37 @@ bool detect_stencil(const int64_t* rp, const int64_t* ci, const double* val, int
         std::memcpy(present, p, sizeof p);
       }
       int64_t k = rp[i];
-      for (int sl = 0; sl < nslot && ok; ++sl) {
+      for (int sl = 0; sl < nslot; ++sl) {
         if (!present[sl]) continue;
-        if (k >= rp[i + 1] || ci[k] != i + off[sl]) {
-          ok = false;
-          break;
-        }
-        if (!have[sl]) {
+        if (k >= rp[i + 1] || ci[k] != i + off[sl]) return false;
+        if (learn && !have[sl]) {
           have[sl] = true;
           cval[sl] = val[k];
         } else if (std::memcmp(&cval[sl], &val[k], sizeof(double)) != 0) {
-          ok = false;
+          return false;
         }
         ++k;
       }
-      if (k != rp[i + 1]) ok = false;
-    }
+      return k == rp[i + 1];
+    };
+    // every slot first occurs within the first g^(dim-1) + g + 1 rows: learn the
+    // values there sequentially, then check all remaining rows in parallel
+    const int64_t learn_rows = std::min<int64_t>(n, (dim == 2 ? g : g2) + g + 1);
+    bool ok = true;
+    for (int64_t i = 0; i < learn_rows && ok; ++i) ok = row_ok(i, true);
     for (int sl = 0; sl < nslot && ok; ++sl)
       if (!have[sl] || !std::isfinite(cval[sl])) ok = false;  // absent-neighbour zeros need finite values
+    if (ok) {
+      std::atomic<bool> all{true};
+      par_rows(n - learn_rows, [&](int64_t lo, int64_t hi) {
+        for (int64_t i = lo + learn_rows; i < hi + learn_rows; ++i)
+          if (!all.load(std::memory_order_relaxed) || !row_ok(i, false)) {
+            all.store(false, std::memory_order_relaxed);
+            return;
+          }
+      });
+      ok = all.load();
+    }
     if (!ok) continue;
     out.dim = dim;
     out.g = g;
@@ -204,16 +295,24 @@ struct DevCsr {
   double* val = nullptr;
 };
 
+// Uploads an operator. detect: look for a grid stencil; a detected stencil is
+// applied matrix-free by every solver kernel, so its CSR is not uploaded unless
+// keep_csr (the plain SpMM entry uses the CSR kernel).
 size_t upload_csr(DevCsr& d, int64_t n, int64_t nnz, const int64_t* rp, const int64_t* ci,
-                  const double* val, cudaStream_t st, bool detect = true) {
+                  const double* val, cudaStream_t st, bool detect = true, bool keep_csr = false) {
   if (n >= (int64_t(1) << 31) || nnz >= (int64_t(1) << 31))
     throw SkError(SK_ERR_UNSUPPORTED, "device CSR uses int32 indices: n and nnz must be < 2^31");
-  std::vector<int32_t> rp32(n + 1), ci32(std::max<int64_t>(nnz, 1));
-  for (int64_t i = 0; i <= n; ++i) rp32[i] = (int32_t)rp[i];
-  for (int64_t k = 0; k < nnz; ++k) ci32[k] = (int32_t)ci[k];
   d.n = n;
   d.nnz = nnz;
   if (detect && !getenv("SK_NO_STENCIL")) detect_stencil(rp, ci, val, n, d.stencil);
+  if (d.stencil.dim && !keep_csr) return 0;
+  std::vector<int32_t> rp32(n + 1), ci32(std::max<int64_t>(nnz, 1));
+  par_rows(n + 1, [&](int64_t lo, int64_t hi) {
+    for (int64_t i = lo; i < hi; ++i) rp32[i] = (int32_t)rp[i];
+  });
+  par_rows(nnz, [&](int64_t lo, int64_t hi) {
+    for (int64_t k = lo; k < hi; ++k) ci32[k] = (int32_t)ci[k];
+  });
   CK(cudaMalloc(&d.rp, sizeof(int32_t) * (n + 1)));
   CK(cudaMalloc(&d.ci, sizeof(int32_t) * std::max<int64_t>(nnz, 1)));
   CK(cudaMalloc(&d.val, sizeof(double) * std::max<int64_t>(nnz, 1)));
@@ -1234,6 +1333,12 @@ void check_device(int dev) {
 size_t upload_local_csr(DevCsr& d, const int64_t* rp, const int64_t* ci, const double* val, int64_t row0,
                         int64_t rows, const StencilInfo& si, cudaStream_t st) {
   const int64_t k0 = rp[row0], k1 = rp[row0 + rows];
+  if (si.dim && !getenv("SK_NO_STENCIL")) {  // matrix-free: no CSR rows needed on the device
+    d.n = rows;
+    d.nnz = k1 - k0;
+    d.stencil = si;
+    return 0;
+  }
   std::vector<int64_t> lrp(rows + 1), lci(std::max<int64_t>(k1 - k0, 1));
   for (int64_t i = 0; i <= rows; ++i) lrp[i] = rp[row0 + i] - k0;
   for (int64_t k = k0; k < k1; ++k) lci[k - k0] = ci[k] - row0;
@@ -1246,26 +1351,47 @@ sk_problem* create_problem(int32_t method, const sk_csr* a, const sk_csr* b, con
                            const double* c2, int64_t s, const sk_gpu_options* gpu, sk::Comm* comm = nullptr) {
   validate_csr(a, "A");
   const bool lyap = method == SK_METHOD_CG_LYAPUNOV;
-  HostCsr bt;  // B^T: the W basis applies it (block_krylov.cpp:54-56)
+  // B^T: the W basis applies it (block_krylov.cpp:54-56). It is formed on the
+  // host only when needed: a bitwise-symmetric B is its own transpose, and the
+  // transpose of a grid stencil is the stencil with mirrored coefficients.
+  HostCsr bt;
+  bool bt_is_b = false;
+  bool bt_mirror = false;
+  StencilInfo bt_st;
+  bool ab_same = false;
   if (lyap) {
     if (a->n_rows != a->n_cols) throw SkError(SK_ERR_DIMENSION, "factorized_cg_lyapunov: A must be square");
-    if (!is_symmetric(a, 1e-12)) throw SkError(SK_ERR_INVALID_MATRIX, "factorized_cg_lyapunov: A is not symmetric");
+    if (!bitwise_symmetric(a) && !is_symmetric(a, 1e-12))
+      throw SkError(SK_ERR_INVALID_MATRIX, "factorized_cg_lyapunov: A is not symmetric");
   } else {
-    const bool ab_same = same_csr(a, b);
+    ab_same = same_csr(a, b);
     if (!ab_same) validate_csr(b, "B");
     if (a->n_rows != a->n_cols || b->n_rows != b->n_cols)
       throw SkError(SK_ERR_DIMENSION, "solver: A and B must be square");
     if (s < 1) throw SkError(SK_ERR_DIMENSION, "solver: C1 and C2 must have the same positive column count");
-    bt = transpose(b);
+    if (bitwise_symmetric(b)) {
+      bt_is_b = true;
+    } else if (method == SK_METHOD_BICGSTAB && !comm && !getenv("SK_NO_STENCIL") &&
+               detect_stencil(b->row_ptr, b->col_idx, b->values, b->n_rows, bt_st)) {
+      bt_mirror = true;  // B^T(i, i+o) = B(i+o, i): slot o takes B's value of slot -o
+      const int ns = bt_st.dim == 2 ? 5 : 7;
+      double c[7];
+      for (int q = 0; q < ns; ++q) c[q] = bt_st.c[ns - 1 - q];
+      for (int q = 0; q < ns; ++q) bt_st.c[q] = c[q];
+    } else {
+      bt = transpose(b);
+    }
     if (method == SK_METHOD_CG) {
-      if (ab_same) {
-        if (!is_symmetric_with(a, bt, 1e-12)) throw SkError(SK_ERR_INVALID_MATRIX, "factorized_cg: A is not symmetric");
-      } else if (!is_symmetric(a, 1e-12)) {
-        throw SkError(SK_ERR_INVALID_MATRIX, "factorized_cg: A is not symmetric");
-      }
-      if (!is_symmetric_with(b, bt, 1e-12)) throw SkError(SK_ERR_INVALID_MATRIX, "factorized_cg: B is not symmetric");
+      const bool a_sym = (ab_same && bt_is_b) || (ab_same ? is_symmetric_with(a, bt, 1e-12)
+                                                          : (bitwise_symmetric(a) || is_symmetric(a, 1e-12)));
+      if (!a_sym) throw SkError(SK_ERR_INVALID_MATRIX, "factorized_cg: A is not symmetric");
+      if (!bt_is_b && !is_symmetric_with(b, bt, 1e-12))
+        throw SkError(SK_ERR_INVALID_MATRIX, "factorized_cg: B is not symmetric");
     }
   }
+  const int64_t* bt_rp = bt_is_b ? b->row_ptr : bt.rp.data();
+  const int64_t* bt_ci = bt_is_b ? b->col_idx : bt.ci.data();
+  const double* bt_val = bt_is_b ? b->values : bt.val.data();
   if (s < 1 || s > a->n_rows) throw SkError(SK_ERR_DIMENSION, "basis init: block size must be in [1, n]");
   if (!lyap && s > b->n_rows) throw SkError(SK_ERR_DIMENSION, "basis init: block size must be in [1, n]");
   if (s > sk::kMaxS) throw SkError(SK_ERR_UNSUPPORTED, "device path supports block sizes s <= 8");
@@ -1299,10 +1425,10 @@ sk_problem* create_problem(int32_t method, const sk_csr* a, const sk_csr* b, con
     p->rank = comm->rank;
     const bool no_st = getenv("SK_NO_STENCIL") != nullptr;
     for (int sd = 0; sd < (lyap ? 1 : 2); ++sd) {
-      const int64_t n = sd == 0 ? a->n_rows : bt.n_rows;
-      const int64_t* rp = sd == 0 ? a->row_ptr : bt.rp.data();
-      const int64_t* ci = sd == 0 ? a->col_idx : bt.ci.data();
-      const double* val = sd == 0 ? a->values : bt.val.data();
+      const int64_t n = sd == 0 ? a->n_rows : b->n_cols;
+      const int64_t* rp = sd == 0 ? a->row_ptr : bt_rp;
+      const int64_t* ci = sd == 0 ? a->col_idx : bt_ci;
+      const double* val = sd == 0 ? a->values : bt_val;
       StencilInfo si;
       if (!no_st) detect_stencil(rp, ci, val, n, si);
       p->plan[sd] = make_plan(n, operator_halo(rp, ci, n, si), p->world);
@@ -1317,12 +1443,15 @@ sk_problem* create_problem(int32_t method, const sk_csr* a, const sk_csr* b, con
   } else {
   p->h2d_bytes += upload_csr(p->op[0], a->n_rows, a->nnz, a->row_ptr, a->col_idx, a->values, p->stream);
   if (!lyap) {
-    if (same_csr(a, bt)) {
+    if (bt_mirror) {  // matrix-free B^T, nothing to upload
+      p->op[1].n = b->n_cols;
+      p->op[1].nnz = b->nnz;
+      p->op[1].stencil = bt_st;
+    } else if (bt_is_b ? ab_same : same_csr(a, bt)) {
       p->op[1] = p->op[0];  // e.g. A = B symmetric: B^T == A bitwise
       p->op_shared = true;
     } else {
-      p->h2d_bytes += upload_csr(p->op[1], bt.n_rows, (int64_t)bt.val.size(), bt.rp.data(),
-                                 bt.ci.data(), bt.val.data(), p->stream);
+      p->h2d_bytes += upload_csr(p->op[1], b->n_cols, b->nnz, bt_rp, bt_ci, bt_val, p->stream);
     }
   }
   }
@@ -1576,11 +1705,11 @@ sk_status sk_spmm(const sk_csr* a, const double* x, int64_t s, int32_t transpose
     int64_t rows, cols;
     if (transpose_flag) {
       t = transpose(a);
-      upload_csr(d, t.n_rows, (int64_t)t.val.size(), t.rp.data(), t.ci.data(), t.val.data(), st);
+      upload_csr(d, t.n_rows, (int64_t)t.val.size(), t.rp.data(), t.ci.data(), t.val.data(), st, true, true);
       rows = a->n_cols;
       cols = a->n_rows;
     } else {
-      upload_csr(d, a->n_rows, a->nnz, a->row_ptr, a->col_idx, a->values, st);
+      upload_csr(d, a->n_rows, a->nnz, a->row_ptr, a->col_idx, a->values, st, true, true);
       rows = a->n_rows;
       cols = a->n_cols;
     }

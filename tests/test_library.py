@@ -76,3 +76,60 @@ def test_input_validation_before_device(skl):
     a = skl.SparseMatrix.identity(3)
     with pytest.raises(skl.DimensionError):
         skl.factorized_cg(a, a, np.ones((4, 1)), np.ones((3, 1)))
+
+
+def _csr_from_dense(skl, d):
+    import scipy.sparse as spx
+    return skl.SparseMatrix.from_scipy(spx.csr_matrix(d))
+
+
+@pytest.mark.parametrize("case", ["decreasing_rowptr", "col_out_of_range", "unsorted_cols"])
+def test_validation_reports_lowest_bad_row(skl, case):
+    """sparse_matrix.cpp:12-32: the parallel host scan reports the error a
+    sequential scan would (lowest offending row), on a matrix large enough to be
+    split across host threads."""
+    n = 300_000
+    rp = np.arange(n + 1, dtype=np.int64)
+    ci = np.arange(n, dtype=np.int64)
+    val = np.ones(n)
+    if case == "decreasing_rowptr":
+        rp = rp.copy(); rp[200_000] = rp[200_001] + 1
+        msg = "not nondecreasing"
+    elif case == "col_out_of_range":
+        ci = ci.copy(); ci[250_000] = n; ci[10_000] = -1
+        msg = "out of range"
+    else:
+        rp = np.concatenate([np.arange(0, 2 * 100, 2), 200 + np.arange(n - 100 + 1)]).astype(np.int64)
+        ci = np.concatenate([np.stack([np.arange(100) + 1, np.arange(100)], 1).ravel(),
+                             np.arange(100, n)]).astype(np.int64)
+        val = np.ones(ci.size)
+        msg = "strictly increasing"
+    a = skl.SparseMatrix(n, n, rp, ci, val)
+    with pytest.raises(skl.InvalidMatrixError, match=msg):
+        skl.factorized_cg(a, a, np.ones((n, 1)), np.ones((n, 1)))
+
+
+def test_symmetry_checks(skl):
+    """Bitwise-symmetric operators skip the transpose; near-symmetric ones (within
+    the reference's 1e-12 relative tolerance) still pass through the full check;
+    nonsymmetric ones are rejected (factorized_solvers.cpp:207-216)."""
+    rng = np.random.default_rng(3)
+    d = rng.standard_normal((40, 40)) * (rng.random((40, 40)) < 0.2) + 10 * np.eye(40)
+    sym = d + d.T
+    near = sym.copy(); near[3, 5] *= 1 + 1e-15
+    expect_cuda = skl.device_count() == 0
+    for mat in (sym, near):
+        a = _csr_from_dense(skl, mat)
+        if expect_cuda:
+            with pytest.raises(skl.CudaError):
+                skl.factorized_cg(a, a, np.ones((40, 1)), np.ones((40, 1)))
+            with pytest.raises(skl.CudaError):
+                skl.factorized_cg_lyapunov(a, np.ones((40, 1)))
+    a = _csr_from_dense(skl, d)
+    with pytest.raises(skl.InvalidMatrixError, match="not symmetric"):
+        skl.factorized_cg(a, a, np.ones((40, 1)), np.ones((40, 1)))
+    with pytest.raises(skl.InvalidMatrixError, match="not symmetric"):
+        skl.factorized_cg_lyapunov(a, np.ones((40, 1)))
+    s = _csr_from_dense(skl, sym)
+    with pytest.raises(skl.InvalidMatrixError, match="B is not symmetric"):
+        skl.factorized_cg(s, a, np.ones((40, 1)), np.ones((40, 1)))
