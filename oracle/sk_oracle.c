@@ -921,6 +921,36 @@ static void cgs_raw(const sko_basis* b, int64_t b0, int64_t b1, double* x, doubl
     free(Ms);
 }
 
+/* Reproducible Lanczos pass (block_krylov.cpp:79-84 in CGS form) with RAW Grams:
+ * Gamma_b = U_b^T z (R1) against the raw operator output z = op U_{k-1}, then
+ * G_b = Gamma_b N_{k-1}^{-1} (each row of Gamma forward-substituted exactly like a
+ * basis row, apply_norm), c_b = N_b^{-T} G_b, M_b = N_b^{-1} c_b, and
+ * w <- w - sum_b U_b M_b with w = z N_{k-1}^{-1}. Raw Grams let the device form
+ * the next extension's Grams in the same sweep that writes U_k, before N_k is
+ * known. */
+static void lanczos_pass_raw(const sko_basis* b, int64_t b0, int64_t b1, const double* z, double* w,
+                             double* c_out) {
+    const int64_t s = b->s, ss = s * s;
+    const double* Nk = nfb(b, b1 - 1);
+    double dinv[64];
+    for (int64_t u = 0; u < s; ++u) dinv[u] = 1.0 / Nk[u * s + u];
+    double* Ms = (double*)xcalloc((size_t)((b1 - b0 + 1) * ss), sizeof(double));
+    for (int64_t jb = b0; jb < b1; ++jb) {
+        double Gam[64 * 64], G[64 * 64];
+        gram(b, ublk(b, jb), z, Gam);
+        for (int64_t t = 0; t < s; ++t) /* row t of Gamma: (Gamma(t,u))_u */
+            for (int64_t u = 0; u < s; ++u) {
+                double acc = Gam[u * s + t];
+                for (int64_t r = 0; r < u; ++r) acc = acc - G[r * s + t] * Nk[u * s + r];
+                G[u * s + t] = acc * dinv[u];
+            }
+        tri_ntinv(nfb(b, jb), G, s, c_out + jb * ss);
+        tri_ninv(nfb(b, jb), c_out + jb * ss, s, Ms + (jb - b0) * ss);
+    }
+    for (int64_t jb = b0; jb < b1; ++jb) sub_vc(b, ublk(b, jb), Ms + (jb - b0) * ss, w);
+    free(Ms);
+}
+
 /* Normalisation of a materialised candidate wx under the reproducible contract:
  * direct R1 Gram -> Cholesky -> sigma extremes; Householder (with R1 dots) when
  * the Gram is not positive definite or sigma_min < 1e-6 sigma_max. */
@@ -1020,14 +1050,14 @@ int sko_basis_try_extend(sko_basis* b) {
     const int64_t n = b->n, s = b->s, k = b->blocks, ss = s * s;
     const int64_t first = b->arnoldi ? 0 : (k - 2 > 0 ? k - 2 : 0);
     double* w = (double*)xcalloc((size_t)(n * s), sizeof(double));
+    double* wr = NULL; /* reproducible: raw operator output z = op U_{k-1} */
     if (b->mode == SKO_REFERENCE_ORDER) {
         basis_apply(b, blk(b, k - 1), w);
     } else {
         /* w = (op U_{k-1}) N_{k-1}^{-1}: raw SpMM, then one row normalisation */
-        double* wr = (double*)xcalloc((size_t)(n * s), sizeof(double));
+        wr = (double*)xcalloc((size_t)(n * s), sizeof(double));
         basis_apply(b, ublk(b, k - 1), wr);
         apply_norm(b, wr, nfb(b, k - 1), w);
-        free(wr);
     }
     double* hcoef = (double*)xcalloc((size_t)(k * ss), sizeof(double)); /* block jb at jb*ss */
     double* q = (double*)xcalloc((size_t)(n * s), sizeof(double));
@@ -1061,7 +1091,10 @@ int sko_basis_try_extend(sko_basis* b) {
     } else {
         /* reproducible contract: CGS pass(es) on the raw blocks, direct CholQR */
         double* cc = (double*)xcalloc((size_t)(k * ss), sizeof(double));
-        cgs_raw(b, first, k, w, hcoef, 1); /* w <- w - V_J c_J */
+        if (b->arnoldi)
+            cgs_raw(b, first, k, w, hcoef, 1); /* w <- w - V_J c_J */
+        else
+            lanczos_pass_raw(b, first, k, wr, w, hcoef);
         if (b->arnoldi || b->full_reorth) {
             /* second CGS pass (Arnoldi: recorded into H; full re-orth: not recorded) */
             cgs_raw(b, 0, k, w, cc, 1);
@@ -1162,6 +1195,7 @@ int sko_basis_try_extend(sko_basis* b) {
         rc = 0;
     }
     free(w);
+    free(wr);
     free(hcoef);
     free(q);
     free(uk);

@@ -502,15 +502,20 @@ __device__ __forceinline__ void stencil_row(const SideConst& sc, const double* _
 // w row (normalised) and the raw own row of U_{k-1}. MODE: 0 CSR, 2/3 stencil
 // (general grid edge), 12/13 stencil with a power-of-two grid edge.
 template <int S, int MODE>
+__device__ __forceinline__ void z_row(const SideConst& sc, const double* __restrict__ x, int64_t i, double* z,
+                                      double* own) {
+  if constexpr (MODE == 2 || MODE == 3)
+    stencil_row<S, MODE, false>(sc, x, i, z, own);
+  else if constexpr (MODE == 12 || MODE == 13)
+    stencil_row<S, MODE - 10, true>(sc, x, i, z, own);
+  else
+    raw_row_csr<S>(sc, x, i, z, own);
+}
+template <int S, int MODE>
 __device__ __forceinline__ void w_row(const SideConst& sc, const double* __restrict__ x, const NF<S>& f,
                                       int64_t i, double* w, double* own) {
   double acc[S];
-  if constexpr (MODE == 2 || MODE == 3)
-    stencil_row<S, MODE, false>(sc, x, i, acc, own);
-  else if constexpr (MODE == 12 || MODE == 13)
-    stencil_row<S, MODE - 10, true>(sc, x, i, acc, own);
-  else
-    raw_row_csr<S>(sc, x, i, acc, own);
+  z_row<S, MODE>(sc, x, i, acc, own);
   norm_row<S>(acc, f, w);
 }
 __device__ __forceinline__ int row_mode(const SideConst& sc) {
@@ -537,15 +542,17 @@ __global__ void __launch_bounds__(256) k_spmm(const __grid_constant__ SolveConst
   const int64_t n = sc.n;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
-    double y[S], own[S];
+    double z[S], y[S], own[S];
     switch (row_mode(sc)) {
-      case 2: w_row<S, 2>(sc, x, f, i, y, own); break;
-      case 3: w_row<S, 3>(sc, x, f, i, y, own); break;
-      case 12: w_row<S, 12>(sc, x, f, i, y, own); break;
-      case 13: w_row<S, 13>(sc, x, f, i, y, own); break;
-      default: w_row<S, 0>(sc, x, f, i, y, own); break;
+      case 2: z_row<S, 2>(sc, x, i, z, own); break;
+      case 3: z_row<S, 3>(sc, x, i, z, own); break;
+      case 12: z_row<S, 12>(sc, x, i, z, own); break;
+      case 13: z_row<S, 13>(sc, x, i, z, own); break;
+      default: z_row<S, 0>(sc, x, i, z, own); break;
     }
+    norm_row<S>(z, f, y);
     st_row<S>(sc.w, i, y);
+    if (!c.arnoldi) st_row<S>(sc.wx, i, z);  // Lanczos Grams are raw
   }
 }
 
@@ -689,7 +696,7 @@ __device__ inline bool gram_setup(const SolveConst& c, int side, int mode, const
   if (ss.exhausted || ss.broken) return false;
   switch (mode) {
     case GM_J:
-      x = sc.w;
+      x = c.arnoldi ? sc.w : sc.wx;  // Lanczos: raw z = op U_{k-1} (k_spmm)
       out = sc.coef;
       mout = sc.mcoef;
       b0 = first_block(c, k);
@@ -768,6 +775,17 @@ __global__ void __launch_bounds__(256) k_gram(const __grid_constant__ SolveConst
     G[e] = tree_stream(sc.part + by * sc.ncta * NB + e, sc.ncta, NB);
   __syncthreads();
   if (threadIdx.x == 0) {
+    if (mode == GM_J && !c.arnoldi) {
+      // raw Gram Gamma_b -> Gamma_b N_{k-1}^{-1}, row by row (as p1_finish)
+      NF<S> fk;
+      load_nf<S>(sc.nfac, c.st->side[side].blocks - 1, fk);
+      for (int t = 0; t < S; ++t) {
+        double row[S], q[S];
+        for (int u = 0; u < S; ++u) row[u] = G[u * S + t];
+        norm_row<S>(row, fk, q);
+        for (int u = 0; u < S; ++u) G[u * S + t] = q[u];
+      }
+    }
     double cb[NB], mb[NB];
     block_coefs(sc.nfac + b * (NB + S), G, S, cb, mb);
     for (int e = 0; e < NB; ++e) {
@@ -803,8 +821,12 @@ __device__ __forceinline__ void p1_body(const SideConst& sc, const double* __res
     const int64_t i = base + lane + 32 * m;
     if (!CHECK || i < n) {
       double y[S], a1[S], a0[S];
-      w_row<S, MODE>(sc, u1, f1, i, y, a1);
-      if (MODE == 0) st_row<S>(sc.w, i, y);
+      z_row<S, MODE>(sc, u1, i, y, a1);  // raw z = op U_{k-1}: the Grams are raw
+      if (MODE == 0) {
+        double w[S];
+        norm_row<S>(y, f1, w);
+        st_row<S>(sc.w, i, w);
+      }
       if (TWO) ld_raw<S>(u0, i, a0);
 #pragma unroll
       for (int u = 0; u < S; ++u)
@@ -830,7 +852,8 @@ __device__ __forceinline__ void p1_dispatch(const SideConst& sc, const double* _
   }
 }
 
-// pass-1 root -> c_b, M_b for blocks k-2 (if any) and k-1
+// pass-1 root (raw Grams Gamma_b = U_b^T z) -> G_b = Gamma_b N_{k-1}^{-1} (each row
+// of Gamma normalised like a basis row) -> c_b, M_b for blocks k-2 (if any), k-1
 template <int S>
 __device__ __noinline__ void p1_finish(const SideConst& sc, int64_t k, const double* res) {
   constexpr int NB = S * S;
@@ -838,8 +861,17 @@ __device__ __noinline__ void p1_finish(const SideConst& sc, int64_t k, const dou
     const int slot = threadIdx.x;  // 0: block k-2, 1: block k-1
     if (slot == 1 || k >= 2) {
       const int64_t b = slot == 0 ? k - 2 : k - 1;
+      NF<S> fk;
+      load_nf<S>(sc.nfac, k - 1, fk);
+      double G[NB];
+      for (int t = 0; t < S; ++t) {
+        double row[S], q[S];
+        for (int u = 0; u < S; ++u) row[u] = res[slot * NB + u * S + t];
+        norm_row<S>(row, fk, q);
+        for (int u = 0; u < S; ++u) G[u * S + t] = q[u];
+      }
       double cb[NB], mb[NB];
-      block_coefs(sc.nfac + b * (NB + S), res + slot * NB, S, cb, mb);
+      block_coefs(sc.nfac + b * (NB + S), G, S, cb, mb);
       for (int e = 0; e < NB; ++e) {
         sc.coef[b * NB + e] = cb[e];
         sc.mcoef[b * NB + e] = mb[e];
