@@ -123,6 +123,9 @@ struct SideConst {
   int64_t chunk_g;           // general-kernel CTAs (32 segments) per reduction chunk
   int64_t nch;               // local reduction chunks
   int64_t halo;              // ghost rows per side of a block (0: none)
+  double* spart;             // wavefront pass: tile partials (self, raw Grams), final scratch
+  unsigned int* sctr;        // wavefront pass: [0] ticket, [1] launch done, [2] side done, [4..] tile flags
+  int64_t bw;                // operator bandwidth max |col - row| (wavefront lag)
   double* hsend;             // [2][halo][s] first / last local rows of the newest block
   double* hrecv;             // [2][halo][s] rows received from the previous / next rank
 };

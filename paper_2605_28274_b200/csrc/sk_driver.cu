@@ -440,6 +440,8 @@ struct SideBuf {
   double *hband = nullptr, *coef = nullptr, *coef2 = nullptr, *part = nullptr, *nfac = nullptr;
   double *mcoef = nullptr, *mcoef2 = nullptr, *hsq = nullptr;
   unsigned int* counter = nullptr;
+  double* spart = nullptr;        // fused sweep scratch (2D stencil sides only)
+  unsigned int* sctr = nullptr;
   double** table = nullptr;
   double** table_host = nullptr;  // pinned mirror (async uploads)
   std::vector<double*> blocks;
@@ -629,6 +631,20 @@ struct Solver {
         sc.sg_pow2 = sh;
       }
       for (int q = 0; q < 7; ++q) sc.scoef[q] = op.stencil.c[q];
+      sc.bw = op.stencil.dim == 2 ? op.stencil.g : (op.stencil.dim == 3 ? op.stencil.g * op.stencil.g : 0);
+      if (!dist && !arnoldi && op.stencil.dim && s <= 4) {
+        // wavefront pass: tile partials (self-Gram, raw Grams), final-tree scratch,
+        // ticket / done counters and per-tile flags (zeroed: no extension yet)
+        const int64_t ne = s * (s + 1) / 2 + 2 * s * s;
+        const int64_t ntile = (nseg + sk::kFusedSegsPerCta - 1) / sk::kFusedSegsPerCta;
+        // (column sweep: segment partials g * g/512, line nodes g, final scratch)
+        const int64_t g = op.stencil.g;
+        const int64_t cols_need = op.stencil.dim == 2 ? (g * (g / sk::kSeg) + g + 2 * (g / 32 + 2)) * ne : 0;
+        b.spart = dalloc<double>(std::max(ntile * ne + 2 * (ntile / 32 + 2) * ne, cols_need) + 64);
+        b.sctr = dalloc<unsigned int>(std::max<int64_t>(ntile, g) + 8);
+      }
+      sc.spart = b.spart;
+      sc.sctr = b.sctr;
       if (dist) setup_partition(sd);
     }
     if (nsides == 1) c.side[1] = c.side[0];
@@ -918,6 +934,13 @@ struct Solver {
     for (int sd = 0; sd < nsides; ++sd) b += 8.0 * P.op[sd].n * s * (J + 1 + (P.op[sd].stencil.dim ? 0 : 1));
     return b;
   }
+  // fused sweep: U_{k-1}, U_{k-2} read and U_k written once per side
+  double sweep_bytes(int64_t k) const {
+    const double J = (double)std::min<int64_t>(k + 1, 2);
+    double b = 0;
+    for (int sd = 0; sd < nsides; ++sd) b += 8.0 * P.op[sd].n * s * (J + 1);
+    return b;
+  }
   // Arnoldi CGS2 extension with kb prior blocks (12nnz + 4(n+1) + 8ns(3kb+5))
   double arnoldi_bytes(int64_t kb) const {
     double b = 0;
@@ -963,6 +986,10 @@ struct Solver {
     // asks for them: pass 2 ends with a pause check, the host sees PAUSED in the
     // status ring, drains the (no-op) run-ahead and runs them for that iteration.
     const bool pause_mode = !arnoldi && !cfg.capture_iterates && !getenv("SK_NO_PAUSE");
+    // fused sweep (pass 2 of extension k + pass 1 of k + 1 in one launch): a
+    // standalone pass 1 runs first and after every rare path (which replaces U_k)
+    const bool sweep = fused && pause_mode && sk::lanczos_sweep_ok(c) && !getenv("SK_NO_SWEEP");
+    bool need_p1 = true;
     auto cg_cores = [&](int64_t k) {
       const double rp = (double)((k + 1) * s), rq = (double)((k + 2) * s);
       timed(4, 8.0 * 3 * rp * rp, [&] { sk::launch_cg_a(c, (k + 1) * s, st); });
@@ -992,7 +1019,15 @@ struct Solver {
       for (int sd = 0; sd < nsides; ++sd) ensure_blocks(sd, k + 2);
       grow_cores((k + 2) * s);
       const double rp = (double)((k + 1) * s), rq = (double)((k + 2) * s);
-      if (fused) {
+      if (sweep) {
+        if (need_p1) {
+          timed(0, pass1_bytes(k), [&] { sk::launch_lanczos_p1(c, st); });
+          dbg("pass1", k);
+          need_p1 = false;
+        }
+        timed(3, sweep_bytes(k), [&] { sk::launch_lanczos_sweep(c, st); });
+        dbg("sweep", k);
+      } else if (fused) {
         timed(0, pass1_bytes(k), [&] { sk::launch_lanczos_p1(c, st); });
         dbg("pass1", k);
         timed(3, pass2_bytes(k), [&] { sk::launch_lanczos_p2(c, st); });
@@ -1050,6 +1085,7 @@ struct Solver {
           timed(2, 0.0, [&] { sk::launch_rare(c, kp + 1, st); });
           dbg("rare", kp);
           cg_cores(kp);
+          need_p1 = true;
           CK(cudaMemcpyAsync(&hstat[kp % RING], &dstate->status, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
           CK(cudaEventRecord(rev[kp % RING], st));
           enq = kp + 1;
@@ -1072,6 +1108,7 @@ struct Solver {
         sk::launch_dist_resume(c, st);
         timed(2, 0.0, [&] { sk::launch_rare(c, hs.k + 1, st); });
         cg_cores(hs.k);
+        need_p1 = true;
         if (read_state().status == sk::RUNNING && hs.k + 1 < max_iter) {
           k_start = hs.k + 1;
           enq = checked = k_start;
@@ -1253,6 +1290,8 @@ struct Solver {
       dfree(b.hsq);
       dfree(b.part);
       dfree(b.counter);
+      dfree(b.spart);
+      dfree(b.sctr);
       dfree(b.table);
       dfree(b.hsend);
       dfree(b.hrecv);

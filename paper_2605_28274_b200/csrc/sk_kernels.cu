@@ -433,7 +433,7 @@ __device__ __forceinline__ void st_row(double* __restrict__ x, int64_t i, const 
 // term v*0 = +-0 leaves the running sum unchanged (the sum starts at +0.0 and
 // never becomes -0.0) -- bitwise the CSR gather that skips it, given finite
 // coefficients (enforced by the host-side detection).
-template <int S, int DIM, bool POW2 = false>
+template <int S, int DIM, bool POW2 = false, bool CGL = false>
 __device__ __forceinline__ void stencil_row(const SideConst& sc, const double* __restrict__ x, int64_t i64,
                                             double* acc, double* own) {
   constexpr int K = DIM == 2 ? 5 : 7;
@@ -483,7 +483,10 @@ __device__ __forceinline__ void stencil_row(const SideConst& sc, const double* _
 #pragma unroll
   for (int k = 0; k < K; ++k) {
     if (pr[k]) {
-      ld_raw<S>(x, col[k], u[k]);
+      if (CGL)
+        ld_raw_cg<S>(x, col[k], u[k]);  // written earlier in the same launch (wavefront pass)
+      else
+        ld_raw<S>(x, col[k], u[k]);
     } else {
 #pragma unroll
       for (int t = 0; t < S; ++t) u[k][t] = 0.0;
@@ -501,13 +504,13 @@ __device__ __forceinline__ void stencil_row(const SideConst& sc, const double* _
 
 // w row (normalised) and the raw own row of U_{k-1}. MODE: 0 CSR, 2/3 stencil
 // (general grid edge), 12/13 stencil with a power-of-two grid edge.
-template <int S, int MODE>
+template <int S, int MODE, bool CGL = false>
 __device__ __forceinline__ void z_row(const SideConst& sc, const double* __restrict__ x, int64_t i, double* z,
                                       double* own) {
   if constexpr (MODE == 2 || MODE == 3)
-    stencil_row<S, MODE, false>(sc, x, i, z, own);
+    stencil_row<S, MODE, false, CGL>(sc, x, i, z, own);
   else if constexpr (MODE == 12 || MODE == 13)
-    stencil_row<S, MODE - 10, true>(sc, x, i, z, own);
+    stencil_row<S, MODE - 10, true, CGL>(sc, x, i, z, own);
   else
     raw_row_csr<S>(sc, x, i, z, own);
 }
@@ -807,11 +810,16 @@ __global__ void __launch_bounds__(256) k_gram(const __grid_constant__ SolveConst
   }
 }
 
+#ifndef SK_WAVE_WARPS
+#define SK_WAVE_WARPS 32  // resident warps / SM for the wavefront pass
+#endif
+constexpr int kWaveBlocks = SK_WAVE_WARPS / kFusedSegsPerCta;
+
 // =====================================================================
 // Fused Lanczos passes (S <= 4). One warp per R1 segment, 8 warps per CTA
 // (the CTA node is the canonical tree's level-3 node).
 // =====================================================================
-template <int S, int MODE, bool TWO, bool CHECK>
+template <int S, int MODE, bool TWO, bool CHECK, bool CGL = false>
 __device__ __forceinline__ void p1_body(const SideConst& sc, const double* __restrict__ u1, const NF<S>& f1,
                                         const double* __restrict__ u0, int64_t base, int64_t n, double* acc) {
   constexpr int NB = S * S;
@@ -821,7 +829,7 @@ __device__ __forceinline__ void p1_body(const SideConst& sc, const double* __res
     const int64_t i = base + lane + 32 * m;
     if (!CHECK || i < n) {
       double y[S], a1[S], a0[S];
-      z_row<S, MODE>(sc, u1, i, y, a1);  // raw z = op U_{k-1}: the Grams are raw
+      z_row<S, MODE, CGL>(sc, u1, i, y, a1);  // raw z = op U_{k-1}: the Grams are raw
       if (MODE == 0) {
         double w[S];
         norm_row<S>(y, f1, w);
@@ -1052,6 +1060,451 @@ __global__ void __launch_bounds__(kFusedThreads, kP2Blocks) k_lanczos_p2(const _
   __shared__ double res[NS];
   final_tree<NS>(sc.part, ncta, res, sc.part + ncta * NS);
   gram_finish<S>(c, side, res, 0);
+}
+
+template <int S>
+__device__ __forceinline__ void sw_put(double* p, const double* v) {
+  if constexpr (S % 2 == 0) {
+#pragma unroll
+    for (int h = 0; h < S / 2; ++h) reinterpret_cast<double2*>(p)[h] = make_double2(v[2 * h], v[2 * h + 1]);
+  } else {
+#pragma unroll
+    for (int t = 0; t < S; ++t) p[t] = v[t];
+  }
+}
+template <int S>
+__device__ __forceinline__ void sw_get(const double* p, double* v) {
+  if constexpr (S % 2 == 0) {
+#pragma unroll
+    for (int h = 0; h < S / 2; ++h) {
+      const double2 q = reinterpret_cast<const double2*>(p)[h];
+      v[2 * h] = q.x;
+      v[2 * h + 1] = q.y;
+    }
+  } else {
+#pragma unroll
+    for (int t = 0; t < S; ++t) v[t] = p[t];
+  }
+}
+
+// =====================================================================
+// Wavefront Lanczos pass (matrix-free stencil operators, one GPU). One launch
+// does pass 2 of extension k AND pass 1 of extension k+1:
+//   phase 1, tile j:     U_k = w - U_{k-2} M_{k-2} - U_{k-1} M_{k-1} on the tile's
+//                        rows (p2_body) + R1 self-Gram; then the tile's flag
+//   phase 2, tile j - D: z' = op U_k on that tile's rows, raw Grams against
+//                        U_{k-1} and U_k (p1_body of extension k+1)
+// Raw Grams need no N_k, so pass 1 of the next extension runs in
+// the same launch, D tiles behind pass 2: D - 1 tiles cover the operator's
+// bandwidth, so every U_k row z' needs is final (flags of lower tiles only).
+// Tiles are handed out in ticket order (atomic counter), so a CTA only ever
+// waits for CTAs that already hold lower tickets: no deadlock. Per side and
+// iteration HBM sees U_{k-1}, U_{k-2} read and U_k written once (3 blocks,
+// against 5 for the two passes); phase 2 re-reads U_k and U_{k-1} from L2.
+// Tile = 8 R1 segments = the CTA partial of the separate-pass kernels, so both
+// reductions are bitwise those of k_lanczos_p2 / k_lanczos_p1.
+// =====================================================================
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_u32(unsigned* p, unsigned v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+// wave geometry of one side: tiles of kFusedSegsPerCta segments, lag D
+struct WaveGeom {
+  int64_t ntile, lag;
+};
+__device__ __forceinline__ WaveGeom wave_geom(const SideConst& sc) {
+  WaveGeom w;
+  w.ntile = (sc.nseg + kFusedSegsPerCta - 1) / kFusedSegsPerCta;
+  const int64_t trows = (int64_t)kSeg * kFusedSegsPerCta;
+  w.lag = 1 + (sc.bw + trows - 1) / trows;
+  return w;
+}
+
+template <int S, int MODE>
+__global__ void __launch_bounds__(kFusedThreads, kWaveBlocks)
+    k_lanczos_wave(const __grid_constant__ SolveConst c, int side0, int interleave) {
+  constexpr int NS = S * (S + 1) / 2, NB = S * S;
+  DevState* st = c.st;
+  if (st->status != RUNNING) return;
+  unsigned* ctl = c.side[side0].sctr;  // [0] ticket, [1] CTAs done (launch-wide)
+  __shared__ unsigned tk;
+  if (threadIdx.x == 0) tk = atomicAdd(ctl, 1u);
+  __syncthreads();
+  const int side = interleave ? side0 + (int)(tk & 1u) : side0;
+  const int64_t j = interleave ? (int64_t)(tk >> 1) : (int64_t)tk;
+  const SideState& ss = st->side[side];
+  const SideConst& sc = c.side[side];
+  const WaveGeom wg = wave_geom(sc);
+  const bool active = !(ss.exhausted || ss.broken) && j < wg.ntile + wg.lag;
+  if (active) {
+    const int64_t k = ss.blocks;
+    const bool two = k >= 2;
+    const unsigned stamp = (unsigned)k;
+    unsigned* flag = sc.sctr + 4;  // per tile: extension whose U_k rows are final
+    double* pself = sc.spart;                         // [ntile][NS]
+    double* pgam = sc.spart + wg.ntile * NS;          // [ntile][2 NB]
+    const double* __restrict__ u1 = sc.blocks[k - 1];
+    const double* __restrict__ u0 = two ? sc.blocks[k - 2] : u1;
+    double* __restrict__ out = sc.blocks[k];
+    const int warp = threadIdx.x >> 5;
+    __shared__ NF<S> f1s;
+    if (j < wg.ntile) {
+      // phase 1: U_k on tile j (pass 2 of extension k)
+      __shared__ double m1[NB], m0[NB];
+      if (threadIdx.x == 0) load_nf<S>(sc.nfac, k - 1, f1s);
+      if (threadIdx.x < NB) {
+        m1[threadIdx.x] = __ldcg(sc.mcoef + (k - 1) * NB + threadIdx.x);
+        m0[threadIdx.x] = two ? __ldcg(sc.mcoef + (k - 2) * NB + threadIdx.x) : 0.0;
+      }
+      __syncthreads();
+      const int64_t seg = j * kFusedSegsPerCta + warp;
+      const int nvalid = (int)mn64(kFusedSegsPerCta, sc.nseg - j * kFusedSegsPerCta);
+      double acc[NS];
+#pragma unroll
+      for (int e = 0; e < NS; ++e) acc[e] = 0.0;
+      if (seg < sc.nseg) p2_dispatch<S, MODE>(sc, u1, f1s, u0, two, m1, m0, out, seg * kSeg, sc.n, acc);
+      warp_seg_to_cta<NS>(acc, nvalid, pself + j * NS);
+      __threadfence();
+      __syncthreads();
+      if (threadIdx.x == 0) st_release_u32(flag + j, stamp);
+    }
+    const int64_t q = j - wg.lag;
+    if (q >= 0) {
+      // phase 2: z' = op U_k on tile q (pass 1 of extension k + 1); the rows of
+      // U_k it reads lie in tiles [q - lag + 1, q + lag - 1], all below j
+      if (threadIdx.x == 0) {
+        const int64_t lo = mx64(0, q - wg.lag + 1), hi = mn64(wg.ntile - 1, q + wg.lag - 1);
+        for (int64_t t = lo; t <= hi; ++t)
+          while (ld_acquire_u32(flag + t) != stamp) __nanosleep(64);
+      }
+      __syncthreads();
+      const int64_t seg = q * kFusedSegsPerCta + warp;
+      const int nvalid = (int)mn64(kFusedSegsPerCta, sc.nseg - q * kFusedSegsPerCta);
+      double acc[2 * NB];
+#pragma unroll
+      for (int e = 0; e < 2 * NB; ++e) acc[e] = 0.0;
+      if (seg < sc.nseg) {
+        const int64_t base = seg * kSeg;  // (f1s: unused by matrix-free rows, no w store)
+        if (base + kSeg <= sc.n)
+          p1_body<S, MODE, true, false, true>(sc, out, f1s, u1, base, sc.n, acc);
+        else
+          p1_body<S, MODE, true, true, true>(sc, out, f1s, u1, base, sc.n, acc);
+      }
+      warp_seg_to_cta<2 * NB>(acc, nvalid, pgam + q * 2 * NB);
+    }
+    // last CTA of this side: both roots, pass-2 finalisation, then pass-1 of k + 1
+    if (last_cta_arrive(sc.sctr + 2, (unsigned)(wg.ntile + wg.lag))) {
+      __shared__ double rself[NS], rgam[2 * NB];
+      double* scratch = sc.spart + wg.ntile * (NS + 2 * NB);
+      final_tree<NS>(pself, wg.ntile, rself, scratch);
+      final_tree<2 * NB>(pgam, wg.ntile, rgam, scratch);
+      gram_finish<S>(c, side, rself, 0);
+      __syncthreads();
+      if (st->side[side].stage == ST_GROW_DIRECT) p1_finish<S>(sc, k + 1, rgam);
+    }
+  }
+  // launch-wide: the last CTA resets the ticket for the next launch
+  if (last_cta_arrive(ctl + 1, gridDim.x)) {
+    if (threadIdx.x == 0) *ctl = 0u;
+  }
+}
+
+// =====================================================================
+// Column sweep (2D grid stencil, g = 512 * 2^j <= 4096, s <= 2, one GPU): the
+// same two passes as the wavefront kernel (pass 2 of extension k + pass 1 of
+// k + 1), organised so that nothing is re-read: one thread per grid column of
+// a 512-column strip walks down a range of grid lines. The two input streams
+// (U_{k-1}, U_{k-2}) arrive in shared-memory line rings by cp.async, issued
+// four lines ahead (so HBM latency never reaches the registers); the U_k lines
+// the stencil needs stay in a three-line shared ring. Out-of-grid neighbours
+// are stored as +0.0, so every row's stencil is the branch-free ascending-
+// column sum of the CSR order.
+// Step y (one __syncthreads): U_k(y) is formed and stored, then z' = op U_k on
+// line y-1; meanwhile three reducer warps form R1 segment partials (lane l
+// sums columns l, l+32, ... sequentially, then the xor butterfly) of the
+// self-Gram of line y-1 and the raw Grams of line y-2 from the rings.
+// A strip's piece of a line is one R1 segment; the last strip CTA of a line
+// range forms the line nodes (aligned groups of nstrip segments) and the last
+// range of a side reduces them and finalises both passes, bitwise as
+// k_lanczos_p2 / k_lanczos_p1.
+// =====================================================================
+#ifndef SK_CS_NC
+#define SK_CS_NC 1
+#endif
+constexpr int kCsNC = SK_CS_NC;            // grid columns per column thread
+constexpr int kCsColWarps = 16 / kCsNC;    // 512 columns
+constexpr int kCsRedWarps = 3;             // self-Gram, raw Gram slot 0, slot 1
+constexpr int kCsThreads = 32 * (kCsColWarps + 1 + kCsRedWarps);
+constexpr int kCsA = kSeg + 4;             // U_{k-1} lines: columns x0-2 .. x0+513
+constexpr int kCsK = kSeg + 2;             // U_k / U_{k-2} lines: columns x0-1 .. x0+512
+constexpr int kCsAR = 8;                   // U_{k-1} ring: lines y-3 .. y+4 (prefetch 4)
+constexpr int kCsBR = 8;                   // U_{k-2} ring: lines y-3 .. y+4 (prefetch 4)
+constexpr int kCsKR = 4;                   // U_k ring: lines y-3 .. y
+constexpr int kCsMaxLines = 4096;
+
+template <int S>
+__device__ __forceinline__ void cs_copy(double* dst, const double* src, bool ok) {
+  if (ok) {
+    const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+    if constexpr (S * 8 == 16)
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(src) : "memory");
+    else
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d), "l"(src) : "memory");
+  } else {
+#pragma unroll
+    for (int t = 0; t < S; ++t) dst[t] = 0.0;
+  }
+}
+__device__ __forceinline__ void cs_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cs_wait3() { asm volatile("cp.async.wait_group 3;" ::: "memory"); }
+// 0 + c0 up + c1 left + c2 centre + c3 right + c4 down (CSR order, mul then add)
+template <int S>
+__device__ __forceinline__ void cs_stencil(const double* c5, const double* up, const double* le, const double* ce,
+                                           const double* ri, const double* dn, double* z) {
+#pragma unroll
+  for (int t = 0; t < S; ++t) {
+    double a = __dadd_rn(0.0, __dmul_rn(c5[0], up[t]));
+    a = __dadd_rn(a, __dmul_rn(c5[1], le[t]));
+    a = __dadd_rn(a, __dmul_rn(c5[2], ce[t]));
+    a = __dadd_rn(a, __dmul_rn(c5[3], ri[t]));
+    z[t] = __dadd_rn(a, __dmul_rn(c5[4], dn[t]));
+  }
+}
+
+template <int S>
+__global__ void __launch_bounds__(kCsThreads, 1)
+    k_lanczos_cols(const __grid_constant__ SolveConst c, int side0, int nranges) {
+  constexpr int NS = S * (S + 1) / 2, NB = S * S, NE = NS + 2 * NB;
+  constexpr int AL = kCsA * S, KL = kCsK * S, ZL = kSeg * S;  // ring line strides (doubles)
+  const int side = side0 + blockIdx.y;
+  if (side >= c.nsides) return;
+  DevState* st = c.st;
+  if (st->status != RUNNING) return;
+  const SideState& ss = st->side[side];
+  if (ss.exhausted || ss.broken) return;
+  const SideConst& sc = c.side[side];
+  const int g = (int)sc.sg;
+  const int nstrip = g / kSeg;
+  const int sx = blockIdx.x % nstrip, rg = blockIdx.x / nstrip;
+  const int y0 = (int)((int64_t)rg * g / nranges), y1 = (int)((int64_t)(rg + 1) * g / nranges);
+  const int x0 = sx * kSeg;
+  const int64_t k = ss.blocks;
+  const bool two = k >= 2;
+  extern __shared__ __align__(16) double cs_smem[];
+  double* Ar = cs_smem;                    // [kCsAR][AL]
+  double* Br = Ar + kCsAR * AL;            // [kCsBR][KL]
+  double* Kb = Br + kCsBR * KL;            // [kCsKR][KL]
+  double* Zs = Kb + kCsKR * KL;            // [2][ZL]
+  __shared__ NF<S> f1s;
+  __shared__ double m1[NB], m0[NB];
+  if (threadIdx.x == 0) load_nf<S>(sc.nfac, k - 1, f1s);
+  if (threadIdx.x < NB) {
+    m1[threadIdx.x] = __ldcg(sc.mcoef + (k - 1) * NB + threadIdx.x);
+    m0[threadIdx.x] = two ? __ldcg(sc.mcoef + (k - 2) * NB + threadIdx.x) : 0.0;
+  }
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t gS = (int64_t)g * S;
+  // column roles: column warp w, lane l owns x0 + 32 w + l + 256 c (c < kCsNC);
+  // the halo warp's lanes 0..3 own x0-1, x0+512 (computed), x0-2, x0+513 (loaded)
+  int xs[kCsNC];
+  bool cv[kCsNC];
+  int nslot = 0;
+  bool compute = false, inner = false;
+  if (warp < kCsColWarps) {
+#pragma unroll
+    for (int q = 0; q < kCsNC; ++q) xs[q] = x0 + 32 * warp + lane + (kSeg / kCsNC) * q;
+    nslot = kCsNC;
+    compute = inner = true;
+  } else if (warp == kCsColWarps && lane < 4) {
+    xs[0] = lane == 0 ? x0 - 1 : lane == 1 ? x0 + kSeg : lane == 2 ? x0 - 2 : x0 + kSeg + 1;
+#pragma unroll
+    for (int q = 1; q < kCsNC; ++q) xs[q] = xs[0];
+    nslot = 1;
+    compute = lane < 2;
+  }
+#pragma unroll
+  for (int q = 0; q < kCsNC; ++q) cv[q] = q < nslot && xs[q] >= 0 && xs[q] < g;
+  const double* U1 = sc.blocks[k - 1];
+  const double* U0 = two ? sc.blocks[k - 2] : U1;
+  double* UK = sc.blocks[k];
+  const int ys = y0 - 1;
+  // copies of line ya of U_{k-1} (and line yb of U_{k-2}) for this thread's columns
+  auto copy_a = [&](int ya) {
+    double* d = Ar + (ya & (kCsAR - 1)) * AL;
+    const bool lok = ya >= 0 && ya < g;
+#pragma unroll
+    for (int q = 0; q < kCsNC; ++q)
+      if (q < nslot) cs_copy<S>(d + (xs[q] - x0 + 2) * S, U1 + ((int64_t)ya * g + (cv[q] ? xs[q] : 0)) * S, lok && cv[q]);
+  };
+  auto copy_b = [&](int yb) {
+    double* d = Br + (yb & (kCsBR - 1)) * KL;
+    const bool lok = two && yb >= 0 && yb < g;
+#pragma unroll
+    for (int q = 0; q < kCsNC; ++q)
+      if (q < nslot) cs_copy<S>(d + (xs[q] - x0 + 1) * S, U0 + ((int64_t)yb * g + (cv[q] ? xs[q] : 0)) * S, lok && cv[q]);
+  };
+  __syncthreads();
+  // prologue: U_{k-1} lines ys-3 .. ys+4, U_{k-2} lines ys .. ys+3 (groups G(ys-4) .. G(ys-1))
+  if (nslot) {
+    for (int ya = ys - 3; ya <= ys; ++ya) copy_a(ya);
+  }
+  for (int v = ys - 4; v < ys; ++v) {
+    if (nslot) copy_a(v + 5);
+    if (compute) copy_b(v + 4);
+    cs_commit();
+  }
+  double* gseg = sc.spart;                              // [g * nstrip][NE] segment partials
+  double* lnode = sc.spart + (int64_t)g * nstrip * NE;  // [g][NE] line nodes
+
+  // steps for lines y0-1 .. y1 (U_k with one halo line each side) + one drain step
+  for (int y = ys; y <= y1 + 1; ++y) {
+    asm volatile("cp.async.wait_group 3;" ::: "memory");
+    __syncthreads();
+    if (warp <= kCsColWarps) {
+      if (compute && y <= y1) {
+        const double* Am = Ar + ((y - 1) & (kCsAR - 1)) * AL;
+        const double* A0 = Ar + (y & (kCsAR - 1)) * AL;
+        const double* Ap = Ar + ((y + 1) & (kCsAR - 1)) * AL;
+        const double* B0 = Br + (y & (kCsBR - 1)) * KL;
+        double* K0 = Kb + (y & (kCsKR - 1)) * KL;
+        const double* K1 = Kb + ((y - 1) & (kCsKR - 1)) * KL;
+        const double* K2 = Kb + ((y - 2) & (kCsKR - 1)) * KL;
+        double* Z1 = Zs + ((y - 1) & 1) * ZL;
+        const bool lin = y >= 0 && y < g;
+        const bool zl = inner && y - 1 >= y0 && y - 1 < y1;
+        const bool wr = inner && y >= y0 && y < y1;
+#pragma unroll
+        for (int q = 0; q < kCsNC; ++q) {
+          if (q < nslot) {
+            const int ai = (xs[q] - x0 + 2) * S, ki = (xs[q] - x0 + 1) * S;
+            double v[S];
+            if (cv[q] && lin) {
+              double up[S], le[S], ce[S], ri[S], dn[S], z[S];
+              sw_get<S>(Am + ai, up);
+              sw_get<S>(A0 + ai - S, le);
+              sw_get<S>(A0 + ai, ce);
+              sw_get<S>(A0 + ai + S, ri);
+              sw_get<S>(Ap + ai, dn);
+              cs_stencil<S>(sc.scoef, up, le, ce, ri, dn, z);
+              norm_row<S>(z, f1s, v);
+              if (two) {
+                double bb[S];
+                sw_get<S>(B0 + ki, bb);
+#pragma unroll
+                for (int u = 0; u < S; ++u) {
+                  double tmp = 0.0;
+#pragma unroll
+                  for (int t = 0; t < S; ++t) tmp = __dadd_rn(tmp, __dmul_rn(bb[t], m0[u * S + t]));
+                  v[u] = __dsub_rn(v[u], tmp);
+                }
+              }
+#pragma unroll
+              for (int u = 0; u < S; ++u) {
+                double tmp = 0.0;
+#pragma unroll
+                for (int t = 0; t < S; ++t) tmp = __dadd_rn(tmp, __dmul_rn(ce[t], m1[u * S + t]));
+                v[u] = __dsub_rn(v[u], tmp);
+              }
+              if (wr) st_row<S>(UK + ((int64_t)y * g + xs[q]) * S, 0, v);
+            } else {
+#pragma unroll
+              for (int t = 0; t < S; ++t) v[t] = 0.0;
+            }
+            sw_put<S>(K0 + ki, v);
+            if (zl) {
+              // z' = op U_k on line y - 1 (own-column values are this thread's writes)
+              double up[S], le[S], ce[S], ri[S], z[S];
+              sw_get<S>(K2 + ki, up);
+              sw_get<S>(K1 + ki - S, le);
+              sw_get<S>(K1 + ki, ce);
+              sw_get<S>(K1 + ki + S, ri);
+              cs_stencil<S>(sc.scoef, up, le, ce, ri, v, z);
+              sw_put<S>(Z1 + (xs[q] - x0) * S, z);
+            }
+          }
+        }
+      }
+      // group G(y): U_{k-1} line y + 5, U_{k-2} line y + 4 (complete at step y + 4)
+      if (nslot) copy_a(y + 5);
+      if (compute) copy_b(y + 4);
+      cs_commit();
+    } else {
+      // reducer warps (R1 lane order): self-Gram of line y-1, raw Grams of line y-2
+      const int r = warp - kCsColWarps - 1;
+      if (r == 0) {
+        const int yl = y - 1;
+        if (yl >= y0 && yl < y1) {
+          const double* K1 = Kb + (yl & (kCsKR - 1)) * KL + S;
+          double acc[NS];
+#pragma unroll
+          for (int e = 0; e < NS; ++e) acc[e] = 0.0;
+#pragma unroll 4
+          for (int m = 0; m < kLRows; ++m) {
+            double vv[S];
+            sw_get<S>(K1 + (lane + 32 * m) * S, vv);
+            int e = 0;
+#pragma unroll
+            for (int u = 0; u < S; ++u)
+#pragma unroll
+              for (int t = 0; t <= u; ++t) {
+                acc[e] = __dadd_rn(acc[e], __dmul_rn(vv[t], vv[u]));
+                ++e;
+              }
+          }
+#pragma unroll
+          for (int e = 0; e < NS; ++e) {
+            const double vv = butterfly(acc[e]);
+            if (lane == e) gseg[((int64_t)yl * nstrip + sx) * NE + e] = vv;
+          }
+        }
+      } else {
+        const int yl = y - 2;
+        if (yl >= y0 && yl < y1) {
+          // slot 0: U_{k-1}(yl) . z'(yl); slot 1: U_k(yl) . z'(yl)
+          const double* src = r == 1 ? Ar + (yl & (kCsAR - 1)) * AL + 2 * S : Kb + (yl & (kCsKR - 1)) * KL + S;
+          const double* Z = Zs + (yl & 1) * ZL;
+          double acc[NB];
+#pragma unroll
+          for (int e = 0; e < NB; ++e) acc[e] = 0.0;
+#pragma unroll 4
+          for (int m = 0; m < kLRows; ++m) {
+            const int cl = lane + 32 * m;
+            double av[S], z[S];
+            sw_get<S>(src + cl * S, av);
+            sw_get<S>(Z + cl * S, z);
+#pragma unroll
+            for (int u = 0; u < S; ++u)
+#pragma unroll
+              for (int t = 0; t < S; ++t) acc[u * S + t] = __dadd_rn(acc[u * S + t], __dmul_rn(av[t], z[u]));
+          }
+#pragma unroll
+          for (int e = 0; e < NB; ++e) {
+            const double vv = butterfly(acc[e]);
+            if (lane == e) gseg[((int64_t)yl * nstrip + sx) * NE + NS + (r - 1) * NB + e] = vv;
+          }
+        }
+      }
+    }
+  }
+  asm volatile("cp.async.wait_all;" ::: "memory");
+  unsigned* ctr = sc.sctr;  // [0..nranges) per range, [nranges] per side
+  if (!last_cta_arrive(ctr + rg, (unsigned)nstrip)) return;
+  for (int idx = threadIdx.x; idx < (y1 - y0) * NE; idx += blockDim.x) {
+    const int l = idx / NE, e = idx - l * NE;
+    double vv[8];
+    for (int q = 0; q < nstrip; ++q) vv[q] = __ldcg(gseg + ((int64_t)(y0 + l) * nstrip + q) * NE + e);
+    lnode[(int64_t)(y0 + l) * NE + e] = tree_reduce_local(vv, nstrip);
+  }
+  if (!last_cta_arrive(ctr + nranges, (unsigned)nranges)) return;
+  __shared__ double res[NE];
+  final_tree<NE>(lnode, g, res, lnode + (int64_t)g * NE);
+  gram_finish<S>(c, side, res, 0);
+  __syncthreads();
+  if (st->side[side].stage == ST_GROW_DIRECT) p1_finish<S>(sc, k + 1, res + NS);
 }
 
 // Clean-up Gram (rare path): each CTA sweeps all blocks for its row group, so
@@ -2155,6 +2608,7 @@ struct Launch {
   static void self_gram(const SolveConst& c, cudaStream_t st);
   static void lanczos_p1(const SolveConst& c, cudaStream_t st);
   static void lanczos_p2(const SolveConst& c, cudaStream_t st);
+  static void lanczos_sweep(const SolveConst& c, cudaStream_t st);
   static void gram_loop(const SolveConst& c, cudaStream_t st);
   static void cg_a(const SolveConst& c, int64_t rmax, cudaStream_t st);
   static void cg_b(const SolveConst& c, int64_t rmax, cudaStream_t st);
@@ -2246,6 +2700,74 @@ struct Launch {
   }
   static void lanczos_p1(const SolveConst& c, cudaStream_t st) { fused(c, 1, st); }
   static void lanczos_p2(const SolveConst& c, cudaStream_t st) { fused(c, 2, st); }
+  static int64_t wave_ctas(const SideConst& sc) {
+    const int64_t ntile = (sc.nseg + kFusedSegsPerCta - 1) / kFusedSegsPerCta;
+    const int64_t trows = (int64_t)kSeg * kFusedSegsPerCta;
+    return ntile + 1 + (sc.bw + trows - 1) / trows;
+  }
+  template <int MODE>
+  static void wave_mode(const SolveConst& c, int side0, int interleave, unsigned grid, cudaStream_t st) {
+    if constexpr (S <= 4 && MODE != 0) k_lanczos_wave<S, MODE><<<grid, kFusedThreads, 0, st>>>(c, side0, interleave);
+  }
+  static void wave_side(const SolveConst& c, int side0, int interleave, unsigned grid, cudaStream_t st) {
+    switch (host_row_mode(c.side[side0])) {
+      case 2: wave_mode<2>(c, side0, interleave, grid, st); break;
+      case 3: wave_mode<3>(c, side0, interleave, grid, st); break;
+      case 12: wave_mode<12>(c, side0, interleave, grid, st); break;
+      case 13: wave_mode<13>(c, side0, interleave, grid, st); break;
+      default: break;
+    }
+  }
+  static bool cols_ok(const SideConst& sc) {
+    if (S > 2 || sc.sdim != 2 || sc.sg % kSeg != 0 || !sc.spart) return false;
+    const int64_t ns = sc.sg / kSeg;
+    return ns <= 8 && (ns & (ns - 1)) == 0;
+  }
+  static int cols_ranges(const SideConst& sc, int nz) {
+    int dev = 0, nsm = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    const int64_t ns = sc.sg / kSeg;
+    int64_t r = nsm / (nz * ns);
+    r = r < 1 ? 1 : r;
+    const int64_t rmin = (sc.sg + kCsMaxLines - 1) / kCsMaxLines;
+    if (r < rmin) r = rmin;
+    if (r > sc.sg) r = sc.sg;
+    return (int)r;
+  }
+  static void cols_launch(const SolveConst& c, int side0, int nz, cudaStream_t st) {
+    if constexpr (S <= 2) {
+      const SideConst& sc = c.side[side0];
+      const int nr = cols_ranges(sc, nz);
+      const size_t smem = sizeof(double) * ((kCsAR * kCsA + (kCsBR + kCsKR) * kCsK + 2 * kSeg) * S);
+      static bool attr = false;
+      if (!attr) {
+        cudaFuncSetAttribute(k_lanczos_cols<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        attr = true;
+      }
+      k_lanczos_cols<S><<<dim3((unsigned)((sc.sg / kSeg) * nr), nz), kCsThreads, smem, st>>>(c, side0, nr);
+    }
+  }
+  static void lanczos_sweep(const SolveConst& c, cudaStream_t st) {
+    if (cols_ok(c.side[0]) && (c.nsides == 1 || cols_ok(c.side[1])) && !getenv("SK_NO_COLS")) {
+      if (c.nsides == 2 && c.side[1].sg != c.side[0].sg) {
+        cols_launch(c, 0, 1, st);
+        cols_launch(c, 1, 1, st);
+      } else {
+        cols_launch(c, 0, c.nsides, st);
+      }
+      return;
+    }
+    const int64_t w0 = wave_ctas(c.side[0]);
+    if (c.nsides == 1) {
+      wave_side(c, 0, 0, (unsigned)w0, st);
+    } else if (wave_ctas(c.side[1]) == w0 && host_row_mode(c.side[1]) == host_row_mode(c.side[0])) {
+      wave_side(c, 0, 1, (unsigned)(2 * w0), st);  // tiles of both sides interleaved
+    } else {
+      wave_side(c, 0, 0, (unsigned)w0, st);
+      wave_side(c, 1, 0, (unsigned)wave_ctas(c.side[1]), st);
+    }
+  }
   static void gram_loop(const SolveConst& c, cudaStream_t st) {
     int64_t nmax, cmax;
     dims(c, nmax, cmax);
@@ -2761,6 +3283,19 @@ void launch_lanczos_p1(const SolveConst& c, cudaStream_t st) {
 void launch_lanczos_p2(const SolveConst& c, cudaStream_t st) {
   SK_DISPATCH_S(c.s, lanczos_p2(c, st));
   g_launches += 1;
+}
+// the wavefront pass applies to matrix-free stencil operators on one GPU
+bool lanczos_sweep_ok(const SolveConst& c) {
+  if (!lanczos_fused_ok(c) || c.arnoldi || c.world > 1) return false;
+  for (int sd = 0; sd < c.nsides; ++sd) {
+    const SideConst& sc = c.side[sd];
+    if (sc.sdim == 0 || sc.dist || sc.row0 != 0 || !sc.spart || !sc.sctr) return false;
+  }
+  return true;
+}
+void launch_lanczos_sweep(const SolveConst& c, cudaStream_t st) {
+  SK_DISPATCH_S(c.s, lanczos_sweep(c, st));
+  g_launches += (c.nsides == 2 && (c.side[1].n != c.side[0].n || c.side[1].sdim != c.side[0].sdim)) ? 2 : 1;
 }
 void launch_lanczos_update(const SolveConst& c, int64_t kmax_blocks, cudaStream_t st) {
   if (c.full_reorth) {

@@ -13,6 +13,8 @@ void launch_lanczos_gram(const SolveConst& c, cudaStream_t st);
 bool lanczos_fused_ok(const SolveConst& c);
 void launch_lanczos_p1(const SolveConst& c, cudaStream_t st);
 void launch_lanczos_p2(const SolveConst& c, cudaStream_t st);
+bool lanczos_sweep_ok(const SolveConst& c);
+void launch_lanczos_sweep(const SolveConst& c, cudaStream_t st);
 void launch_lanczos_update(const SolveConst& c, int64_t kmax_blocks, cudaStream_t st);
 void launch_rare(const SolveConst& c, int64_t kmax_blocks, cudaStream_t st);
 void launch_arnoldi_ext(const SolveConst& c, int64_t kmax_blocks, cudaStream_t st);
