@@ -51,6 +51,18 @@ struct HostCsr {
   std::vector<double> val;
 };
 
+// SK_TRACE=1: host phase timings of the e2e path on stderr
+struct HostTrace {
+  bool on = getenv("SK_TRACE") != nullptr;
+  std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
+  void mark(const char* what) {
+    if (!on) return;
+    const auto n = std::chrono::steady_clock::now();
+    fprintf(stderr, "[sk] %-28s %8.2f ms\n", what, std::chrono::duration<double, std::milli>(n - t).count());
+    t = n;
+  }
+};
+
 // Host row loops run on all host threads (the e2e path validates and inspects
 // CSRs of up to 84M entries per call). f(lo, hi) gets a contiguous row range.
 int host_threads() {
@@ -62,8 +74,8 @@ int host_threads() {
   return t;
 }
 template <class F>
-void par_rows(int64_t n, F&& f) {
-  const int T = (int)std::min<int64_t>(host_threads(), std::max<int64_t>(1, n / 65536));
+void par_rows(int64_t n, F&& f, int64_t min_rows = 65536) {
+  const int T = (int)std::min<int64_t>(host_threads(), std::max<int64_t>(1, n / min_rows));
   if (T <= 1) {
     f(int64_t(0), n);
     return;
@@ -235,9 +247,8 @@ bool detect_stencil(const int64_t* rp, const int64_t* ci, const double* val, int
     }
     bool have[7] = {false, false, false, false, false, false, false};
     double cval[7] = {0, 0, 0, 0, 0, 0, 0};
-    // row i matches the stencil; learn = adopt a slot's first value seen
-    auto row_ok = [&](int64_t i, bool learn) {
-      const int64_t ix = i % g, iy = (i / g) % g, iz = i / g2;
+    // row i (grid point ix, iy, iz) matches the stencil; learn = adopt a slot's first value seen
+    auto row_ok = [&](int64_t i, int64_t ix, int64_t iy, int64_t iz, bool learn) {
       bool present[7];
       if (dim == 2) {
         const bool p[5] = {iy > 0, ix > 0, true, ix < g - 1, iy < g - 1};
@@ -264,17 +275,28 @@ bool detect_stencil(const int64_t* rp, const int64_t* ci, const double* val, int
     // values there sequentially, then check all remaining rows in parallel
     const int64_t learn_rows = std::min<int64_t>(n, (dim == 2 ? g : g2) + g + 1);
     bool ok = true;
-    for (int64_t i = 0; i < learn_rows && ok; ++i) ok = row_ok(i, true);
+    for (int64_t i = 0; i < learn_rows && ok; ++i) ok = row_ok(i, i % g, (i / g) % g, i / g2, true);
     for (int sl = 0; sl < nslot && ok; ++sl)
       if (!have[sl] || !std::isfinite(cval[sl])) ok = false;  // absent-neighbour zeros need finite values
     if (ok) {
       std::atomic<bool> all{true};
       par_rows(n - learn_rows, [&](int64_t lo, int64_t hi) {
-        for (int64_t i = lo + learn_rows; i < hi + learn_rows; ++i)
-          if (!all.load(std::memory_order_relaxed) || !row_ok(i, false)) {
+        const int64_t i0 = lo + learn_rows;
+        int64_t ix = i0 % g, iy = (i0 / g) % g, iz = i0 / g2;
+        for (int64_t i = i0; i < hi + learn_rows; ++i) {
+          if (!row_ok(i, ix, iy, iz, false)) {
             all.store(false, std::memory_order_relaxed);
             return;
           }
+          if (++ix == g) {
+            ix = 0;
+            if (++iy == g) {
+              iy = 0;
+              ++iz;
+            }
+            if (!all.load(std::memory_order_relaxed)) return;
+          }
+        }
       });
       ok = all.load();
     }
@@ -285,6 +307,48 @@ bool detect_stencil(const int64_t* rp, const int64_t* ci, const double* val, int
     return true;
   }
   return false;
+}
+
+// a detected grid stencil is bitwise symmetric iff its offsets' values mirror
+// (c(-o) == c(o)): then the CSR equals its transpose entry for entry
+bool stencil_symmetric(const StencilInfo& si) {
+  const int ns = si.dim == 2 ? 5 : 7;
+  for (int q = 0; q < ns; ++q)
+    if (std::memcmp(&si.c[q], &si.c[ns - 1 - q], sizeof(double)) != 0) return false;
+  return si.dim != 0;
+}
+
+// Host -> device copy of caller (pageable) memory through two pinned staging
+// buffers: chunk i is copied into buffer i % 2 by all host threads while chunk
+// i - 1 is in flight on the stream (the staging buffers live for the process).
+void h2d_staged(void* dst, const void* src, size_t bytes, cudaStream_t st) {
+  constexpr size_t kChunk = size_t(32) << 20;
+  static std::mutex mu;
+  static char* stage[2] = {nullptr, nullptr};
+  static cudaEvent_t done[2];
+  std::lock_guard<std::mutex> g(mu);
+  if (!stage[0]) {
+    for (int b = 0; b < 2; ++b) {
+      if (cudaHostAlloc(&stage[b], kChunk, cudaHostAllocDefault) != cudaSuccess) {
+        stage[0] = stage[1] = nullptr;
+        CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, st));
+        return;
+      }
+      CK(cudaEventCreateWithFlags(&done[b], cudaEventDisableTiming));
+      CK(cudaEventRecord(done[b], st));
+    }
+  }
+  for (size_t off = 0, i = 0; off < bytes; off += kChunk, ++i) {
+    const size_t n = std::min(kChunk, bytes - off);
+    char* buf = stage[i & 1];
+    CK(cudaEventSynchronize(done[i & 1]));
+    par_rows((int64_t)(n / 4096) + 1, [&](int64_t lo, int64_t hi) {
+      const size_t a = std::min(n, (size_t)lo * 4096), b = std::min(n, (size_t)hi * 4096);
+      if (b > a) std::memcpy(buf + a, (const char*)src + off + a, b - a);
+    }, 256);
+    CK(cudaMemcpyAsync((char*)dst + off, buf, n, cudaMemcpyHostToDevice, st));
+    CK(cudaEventRecord(done[i & 1], st));
+  }
 }
 
 struct DevCsr {
@@ -299,12 +363,16 @@ struct DevCsr {
 // applied matrix-free by every solver kernel, so its CSR is not uploaded unless
 // keep_csr (the plain SpMM entry uses the CSR kernel).
 size_t upload_csr(DevCsr& d, int64_t n, int64_t nnz, const int64_t* rp, const int64_t* ci,
-                  const double* val, cudaStream_t st, bool detect = true, bool keep_csr = false) {
+                  const double* val, cudaStream_t st, bool detect = true, bool keep_csr = false,
+                  const StencilInfo* pre = nullptr) {
   if (n >= (int64_t(1) << 31) || nnz >= (int64_t(1) << 31))
     throw SkError(SK_ERR_UNSUPPORTED, "device CSR uses int32 indices: n and nnz must be < 2^31");
   d.n = n;
   d.nnz = nnz;
-  if (detect && !getenv("SK_NO_STENCIL")) detect_stencil(rp, ci, val, n, d.stencil);
+  if (pre)
+    d.stencil = *pre;
+  else if (detect && !getenv("SK_NO_STENCIL"))
+    detect_stencil(rp, ci, val, n, d.stencil);
   if (d.stencil.dim && !keep_csr) return 0;
   std::vector<int32_t> rp32(n + 1), ci32(std::max<int64_t>(nnz, 1));
   par_rows(n + 1, [&](int64_t lo, int64_t hi) {
@@ -955,7 +1023,9 @@ struct Solver {
   }
 
   sk_solution* run() {
+    HostTrace tr;
     setup();
+    tr.mark("  setup (allocations)");
     if (dist) return run_dist();
     cudaEvent_t t0, t1;
     CK(cudaEventCreate(&t0));
@@ -1128,8 +1198,10 @@ struct Solver {
     cudaFreeHost(hstat);
     for (auto e : pool) cudaEventDestroy(e);
     pool.clear();
-
-    return make_solution(ms, std::move(caps), std::move(cap_shape));
+    tr.mark("  device loop");
+    sk_solution* sol = make_solution(ms, std::move(caps), std::move(cap_shape));
+    tr.mark("  solution (D2H history)");
+    return sol;
   }
 
   sk_solution* make_solution(float ms, std::vector<std::vector<double>> caps,
@@ -1388,8 +1460,44 @@ size_t upload_local_csr(DevCsr& d, const int64_t* rp, const int64_t* ci, const d
 
 sk_problem* create_problem(int32_t method, const sk_csr* a, const sk_csr* b, const double* c1,
                            const double* c2, int64_t s, const sk_gpu_options* gpu, sk::Comm* comm = nullptr) {
-  validate_csr(a, "A");
+  HostTrace tr;
   const bool lyap = method == SK_METHOD_CG_LYAPUNOV;
+  // C1/C2 go to the device on a helper thread while the host checks run (the
+  // buffers are released if a check throws)
+  struct EarlyH2D {
+    std::thread th;
+    double* d1 = nullptr;
+    double* d2 = nullptr;
+    cudaStream_t st = nullptr;
+    std::string err;
+    ~EarlyH2D() {
+      if (th.joinable()) th.join();
+      if (d1) cudaFree(d1);
+      if (d2) cudaFree(d2);
+      if (st) cudaStreamDestroy(st);
+    }
+  } early;
+  const int dev0 = gpu ? gpu->device : 0;
+  int ndev = 0;
+  if (!comm && a && c1 && (lyap || (b && c2)) && s >= 1 && s <= sk::kMaxS && a->n_rows > 0 &&
+      cudaGetDeviceCount(&ndev) == cudaSuccess && dev0 >= 0 && dev0 < ndev && cudaSetDevice(dev0) == cudaSuccess) {
+    const size_t b1 = sizeof(double) * a->n_rows * s, b2 = lyap ? 0 : sizeof(double) * b->n_rows * s;
+    if (cudaStreamCreateWithFlags(&early.st, cudaStreamNonBlocking) == cudaSuccess &&
+        cudaMalloc(&early.d1, b1) == cudaSuccess && (lyap || cudaMalloc(&early.d2, b2) == cudaSuccess)) {
+      early.th = std::thread([&early, c1, c2, b1, b2, dev0] {
+        try {
+          CK(cudaSetDevice(dev0));
+          h2d_staged(early.d1, c1, b1, early.st);
+          if (early.d2) h2d_staged(early.d2, c2, b2, early.st);
+          CK(cudaStreamSynchronize(early.st));
+        } catch (const std::exception& e) {
+          early.err = e.what();
+        }
+      });
+    }
+  }
+  validate_csr(a, "A");
+  tr.mark("validate A");
   // B^T: the W basis applies it (block_krylov.cpp:54-56). It is formed on the
   // host only when needed: a bitwise-symmetric B is its own transpose, and the
   // transpose of a grid stencil is the stencil with mirrored coefficients.
@@ -1398,9 +1506,16 @@ sk_problem* create_problem(int32_t method, const sk_csr* a, const sk_csr* b, con
   bool bt_mirror = false;
   StencilInfo bt_st;
   bool ab_same = false;
+  // grid stencils are detected once, up front (a linear pass): a mirror-symmetric
+  // stencil is bitwise symmetric without the per-entry search
+  const bool use_st = !getenv("SK_NO_STENCIL");
+  StencilInfo st_a, st_b;
+  if (use_st) detect_stencil(a->row_ptr, a->col_idx, a->values, a->n_rows, st_a);
+  auto sym_a = [&] { return stencil_symmetric(st_a) || bitwise_symmetric(a); };
+  tr.mark("stencil detection A");
   if (lyap) {
     if (a->n_rows != a->n_cols) throw SkError(SK_ERR_DIMENSION, "factorized_cg_lyapunov: A must be square");
-    if (!bitwise_symmetric(a) && !is_symmetric(a, 1e-12))
+    if (!sym_a() && !is_symmetric(a, 1e-12))
       throw SkError(SK_ERR_INVALID_MATRIX, "factorized_cg_lyapunov: A is not symmetric");
   } else {
     ab_same = same_csr(a, b);
@@ -1408,26 +1523,29 @@ sk_problem* create_problem(int32_t method, const sk_csr* a, const sk_csr* b, con
     if (a->n_rows != a->n_cols || b->n_rows != b->n_cols)
       throw SkError(SK_ERR_DIMENSION, "solver: A and B must be square");
     if (s < 1) throw SkError(SK_ERR_DIMENSION, "solver: C1 and C2 must have the same positive column count");
-    if (bitwise_symmetric(b)) {
+    if (ab_same)
+      st_b = st_a;
+    else if (use_st)
+      detect_stencil(b->row_ptr, b->col_idx, b->values, b->n_rows, st_b);
+    if (stencil_symmetric(st_b) || bitwise_symmetric(b)) {
       bt_is_b = true;
-    } else if (method == SK_METHOD_BICGSTAB && !comm && !getenv("SK_NO_STENCIL") &&
-               detect_stencil(b->row_ptr, b->col_idx, b->values, b->n_rows, bt_st)) {
+    } else if (method == SK_METHOD_BICGSTAB && !comm && st_b.dim) {
       bt_mirror = true;  // B^T(i, i+o) = B(i+o, i): slot o takes B's value of slot -o
+      bt_st = st_b;
       const int ns = bt_st.dim == 2 ? 5 : 7;
-      double c[7];
-      for (int q = 0; q < ns; ++q) c[q] = bt_st.c[ns - 1 - q];
-      for (int q = 0; q < ns; ++q) bt_st.c[q] = c[q];
+      for (int q = 0; q < ns; ++q) bt_st.c[q] = st_b.c[ns - 1 - q];
     } else {
       bt = transpose(b);
     }
     if (method == SK_METHOD_CG) {
       const bool a_sym = (ab_same && bt_is_b) || (ab_same ? is_symmetric_with(a, bt, 1e-12)
-                                                          : (bitwise_symmetric(a) || is_symmetric(a, 1e-12)));
+                                                          : (sym_a() || is_symmetric(a, 1e-12)));
       if (!a_sym) throw SkError(SK_ERR_INVALID_MATRIX, "factorized_cg: A is not symmetric");
       if (!bt_is_b && !is_symmetric_with(b, bt, 1e-12))
         throw SkError(SK_ERR_INVALID_MATRIX, "factorized_cg: B is not symmetric");
     }
   }
+  tr.mark("symmetry / B^T");
   const int64_t* bt_rp = bt_is_b ? b->row_ptr : bt.rp.data();
   const int64_t* bt_ci = bt_is_b ? b->col_idx : bt.ci.data();
   const double* bt_val = bt_is_b ? b->values : bt.val.data();
@@ -1437,6 +1555,7 @@ sk_problem* create_problem(int32_t method, const sk_csr* a, const sk_csr* b, con
   if (!c1 || (!lyap && !c2)) throw SkError(SK_ERR_DIMENSION, "solver: C1/C2 missing");
   const int dev = gpu ? gpu->device : 0;
   check_device(dev);
+  tr.mark("device check");
   auto p = std::make_unique<sk_problem>();
   p->method = method;
   p->s = s;
@@ -1480,7 +1599,8 @@ sk_problem* create_problem(int32_t method, const sk_csr* a, const sk_csr* b, con
       p->nglob[1] = p->nglob[0];
     }
   } else {
-  p->h2d_bytes += upload_csr(p->op[0], a->n_rows, a->nnz, a->row_ptr, a->col_idx, a->values, p->stream);
+  p->h2d_bytes += upload_csr(p->op[0], a->n_rows, a->nnz, a->row_ptr, a->col_idx, a->values, p->stream, true,
+                             false, use_st ? &st_a : nullptr);
   if (!lyap) {
     if (bt_mirror) {  // matrix-free B^T, nothing to upload
       p->op[1].n = b->n_cols;
@@ -1490,19 +1610,29 @@ sk_problem* create_problem(int32_t method, const sk_csr* a, const sk_csr* b, con
       p->op[1] = p->op[0];  // e.g. A = B symmetric: B^T == A bitwise
       p->op_shared = true;
     } else {
-      p->h2d_bytes += upload_csr(p->op[1], b->n_cols, b->nnz, bt_rp, bt_ci, bt_val, p->stream);
+      p->h2d_bytes += upload_csr(p->op[1], b->n_cols, b->nnz, bt_rp, bt_ci, bt_val, p->stream, true, false,
+                                 (bt_is_b && use_st) ? &st_b : nullptr);
     }
   }
   }
-  CK(cudaMalloc(&p->c1, sizeof(double) * p->n * s));
-  CK(cudaMemcpyAsync(p->c1, c1, sizeof(double) * p->n * s, cudaMemcpyHostToDevice, p->stream));
-  p->h2d_bytes += sizeof(double) * p->n * s;
-  if (!lyap) {
-    CK(cudaMalloc(&p->c2, sizeof(double) * p->m * s));
-    CK(cudaMemcpyAsync(p->c2, c2, sizeof(double) * p->m * s, cudaMemcpyHostToDevice, p->stream));
-    p->h2d_bytes += sizeof(double) * p->m * s;
+  tr.mark("operators (detect/upload)");
+  if (early.th.joinable()) early.th.join();
+  if (!early.err.empty()) throw SkError(SK_ERR_CUDA, early.err);
+  if (early.d1) {  // uploaded while the checks ran
+    p->c1 = early.d1;
+    p->c2 = early.d2;
+    early.d1 = early.d2 = nullptr;
+  } else {
+    CK(cudaMalloc(&p->c1, sizeof(double) * p->n * s));
+    h2d_staged(p->c1, c1, sizeof(double) * p->n * s, p->stream);
+    if (!lyap) {
+      CK(cudaMalloc(&p->c2, sizeof(double) * p->m * s));
+      h2d_staged(p->c2, c2, sizeof(double) * p->m * s, p->stream);
+    }
   }
+  p->h2d_bytes += sizeof(double) * p->n * s + (lyap ? 0 : sizeof(double) * p->m * s);
   CK(cudaStreamSynchronize(p->stream));
+  tr.mark("C1/C2 H2D (wait)");
   p->h2d_time = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
   return p.release();
 }
@@ -1571,8 +1701,10 @@ sk_status sk_problem_solve(sk_problem* p, const sk_config* cfg, sk_solution** ou
   return run_guarded([&] {
     if (!p) throw SkError(SK_ERR_DIMENSION, "null problem");
     CK(cudaSetDevice(p->device));
+    HostTrace tr;
     Solver solver(*p, default_cfg(cfg));
     *out = solver.run();
+    tr.mark("solve (setup+device+D2H)");
   });
 }
 
