@@ -1374,26 +1374,41 @@ __global__ void __launch_bounds__(kCsThreads, 1)
         const double* K1 = Kb + ((y - 1) & (kCsKR - 1)) * KL;
         const double* K2 = Kb + ((y - 2) & (kCsKR - 1)) * KL;
         double* Z1 = Zs + ((y - 1) & 1) * ZL;
-        const bool lin = y >= 0 && y < g;
         const bool zl = inner && y - 1 >= y0 && y - 1 < y1;
         const bool wr = inner && y >= y0 && y < y1;
 #pragma unroll
         for (int q = 0; q < kCsNC; ++q) {
           if (q < nslot) {
+            // branch-free; a point outside the grid (halo line / column) is zeroed
+            // after the fact (its stencil sees in-grid neighbours)
             const int ai = (xs[q] - x0 + 2) * S, ki = (xs[q] - x0 + 1) * S;
-            double v[S];
-            if (cv[q] && lin) {
-              double up[S], le[S], ce[S], ri[S], dn[S], z[S];
+            double v[S], z2[S];
+            {
+              double up[S], le[S], ce[S], ri[S];
+              sw_get<S>(K2 + ki, up);
+              sw_get<S>(K1 + ki - S, le);
+              sw_get<S>(K1 + ki, ce);
+              sw_get<S>(K1 + ki + S, ri);
+              // z' = op U_k on line y - 1: the first four terms, the down term below
+#pragma unroll
+              for (int t = 0; t < S; ++t) {
+                double a2 = __dadd_rn(0.0, __dmul_rn(sc.scoef[0], up[t]));
+                a2 = __dadd_rn(a2, __dmul_rn(sc.scoef[1], le[t]));
+                a2 = __dadd_rn(a2, __dmul_rn(sc.scoef[2], ce[t]));
+                z2[t] = __dadd_rn(a2, __dmul_rn(sc.scoef[3], ri[t]));
+              }
+            }
+            {
+              double up[S], le[S], ce[S], ri[S], dn[S], z[S], bb[S];
               sw_get<S>(Am + ai, up);
               sw_get<S>(A0 + ai - S, le);
               sw_get<S>(A0 + ai, ce);
               sw_get<S>(A0 + ai + S, ri);
               sw_get<S>(Ap + ai, dn);
+              sw_get<S>(B0 + ki, bb);
               cs_stencil<S>(sc.scoef, up, le, ce, ri, dn, z);
               norm_row<S>(z, f1s, v);
               if (two) {
-                double bb[S];
-                sw_get<S>(B0 + ki, bb);
 #pragma unroll
                 for (int u = 0; u < S; ++u) {
                   double tmp = 0.0;
@@ -1409,21 +1424,17 @@ __global__ void __launch_bounds__(kCsThreads, 1)
                 for (int t = 0; t < S; ++t) tmp = __dadd_rn(tmp, __dmul_rn(ce[t], m1[u * S + t]));
                 v[u] = __dsub_rn(v[u], tmp);
               }
-              if (wr) st_row<S>(UK + ((int64_t)y * g + xs[q]) * S, 0, v);
-            } else {
+            }
+            if (!(cv[q] && y >= 0 && y < g)) {
 #pragma unroll
               for (int t = 0; t < S; ++t) v[t] = 0.0;
             }
+            if (wr) st_row<S>(UK + ((int64_t)y * g + xs[q]) * S, 0, v);
             sw_put<S>(K0 + ki, v);
             if (zl) {
-              // z' = op U_k on line y - 1 (own-column values are this thread's writes)
-              double up[S], le[S], ce[S], ri[S], z[S];
-              sw_get<S>(K2 + ki, up);
-              sw_get<S>(K1 + ki - S, le);
-              sw_get<S>(K1 + ki, ce);
-              sw_get<S>(K1 + ki + S, ri);
-              cs_stencil<S>(sc.scoef, up, le, ce, ri, v, z);
-              sw_put<S>(Z1 + (xs[q] - x0) * S, z);
+#pragma unroll
+              for (int t = 0; t < S; ++t) z2[t] = __dadd_rn(z2[t], __dmul_rn(sc.scoef[4], v[t]));
+              sw_put<S>(Z1 + (xs[q] - x0) * S, z2);
             }
           }
         }
