@@ -167,6 +167,23 @@ const char* sk_last_error(void);
 const char* sk_version(void);
 int32_t sk_device_count(void);
 
+/* True residual ||A X + X B - C1 C2^T||_F / ||C1 C2^T||_F of X = V core W^T on the
+ * device (replaces true_residual / true_residual_factors, factorized_solvers.hpp:56-61,
+ * factorized_solvers.cpp:391-444): the R factors of [C1, A V core, V core] and
+ * [C2, W, B^T W] by a streaming TSQR (the stacked factors are never formed), the
+ * residual core R_U diag(I, -I, -I) R_V^T reduced on the host. Floating point, not
+ * the bitwise contract. Errors as the reference: SK_ERR_DIMENSION for shapes,
+ * SK_ERR_INVALID_MATRIX for a zero right-hand side. sk_true_residual reads V, core
+ * and W where the solution holds them (HBM); sk_true_residual_factors takes host
+ * column-major factors (n x rv, rv x rw, m x rw); sk_problem_true_residual uses the
+ * problem's resident operators and C1/C2 (Lyapunov: B = A, C2 = C1). */
+sk_status sk_true_residual(const sk_csr* a, const sk_csr* b, const double* c1, const double* c2, int64_t s,
+                           const sk_solution* sol, double* rel);
+sk_status sk_true_residual_factors(const sk_csr* a, const sk_csr* b, const double* c1, const double* c2,
+                                   int64_t s, const double* v, int64_t rv, const double* core,
+                                   const double* w, int64_t rw, double* rel);
+sk_status sk_problem_true_residual(const sk_problem* p, const sk_solution* sol, double* rel);
+
 /* Kernel-level entry for parity tests: y = A x (reference spmm order) or
  * y = A^T x (spmm_transpose, via the transposed CSR) on the device. */
 sk_status sk_spmm(const sk_csr* a, const double* x, int64_t s, int32_t transpose, double* y);

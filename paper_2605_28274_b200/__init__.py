@@ -374,6 +374,13 @@ class ResidentProblem:
         _check(lib().sk_problem_solve(self._h, C.byref(cfg_c), C.byref(h)))
         return FactorizedSolution(h)
 
+    def true_residual(self, sol: FactorizedSolution) -> float:
+        """Device true residual of `sol` against this problem's resident operators and
+        right-hand side (factorized_solvers.cpp:441-444; sk_problem_true_residual)."""
+        out = C.c_double()
+        _check(lib().sk_problem_true_residual(self._h, sol._h, C.byref(out)))
+        return out.value
+
     def free(self):
         if getattr(self, "_h", None):
             lib().sk_problem_free(self._h)
@@ -384,6 +391,40 @@ class ResidentProblem:
             self.free()
         except Exception:
             pass
+
+
+def true_residual(a: SparseMatrix, b: SparseMatrix, c1, c2, sol: FactorizedSolution) -> float:
+    """true_residual (factorized_solvers.hpp:56-57) on the device: the solution's V,
+    core and W are read where they live (HBM)."""
+    c1 = _mat(c1, a.n_rows, "C1")
+    c2 = _mat(c2, b.n_rows, "C2")
+    if c1.shape[1] != c2.shape[1]:
+        raise DimensionError("true_residual: right-hand side shapes do not conform")
+    ca, cb = a._c(), b._c()
+    out = C.c_double()
+    _check(lib().sk_true_residual(C.byref(ca), C.byref(cb), _p(c1), _p(c2), C.c_int64(c1.shape[1]),
+                                  sol._h, C.byref(out)))
+    return out.value
+
+
+def true_residual_factors(a: SparseMatrix, b: SparseMatrix, c1, c2, v, core, w) -> float:
+    """true_residual_factors (factorized_solvers.hpp:59-61) on the device for host factors."""
+    c1 = _mat(c1, a.n_rows, "C1")
+    c2 = _mat(c2, b.n_rows, "C2")
+    v = np.asfortranarray(np.asarray(v, dtype=np.float64))
+    core = np.asfortranarray(np.asarray(core, dtype=np.float64))
+    w = np.asfortranarray(np.asarray(w, dtype=np.float64))
+    if c1.shape[1] != c2.shape[1]:
+        raise DimensionError("true_residual: right-hand side shapes do not conform")
+    if (v.ndim != 2 or core.ndim != 2 or w.ndim != 2 or v.shape[0] != a.n_rows or w.shape[0] != b.n_rows
+            or core.shape != (v.shape[1], w.shape[1])):
+        raise DimensionError("true_residual: factor shapes do not conform")
+    ca, cb = a._c(), b._c()
+    out = C.c_double()
+    _check(lib().sk_true_residual_factors(C.byref(ca), C.byref(cb), _p(c1), _p(c2), C.c_int64(c1.shape[1]),
+                                          _p(v), C.c_int64(v.shape[1]), _p(core), _p(w),
+                                          C.c_int64(w.shape[1]), C.byref(out)))
+    return out.value
 
 
 def spmm(a: SparseMatrix, x, transpose: bool = False) -> np.ndarray:

@@ -30,6 +30,7 @@ def units():
     u = [("sk_kernels.cu", f"sk_kernels_s{s}.o", [f"-DSK_INST_S={s}"]) for s in S_VALUES]
     u.append(("sk_kernels.cu", "sk_kernels_common.o", ["-DSK_INST_COMMON"]))
     u.append(("sk_driver.cu", "sk_driver.o", []))
+    u.append(("sk_residual.cu", "sk_residual.o", []))
     u.append(("sk_problems.cpp", "sk_problems.o", []))
     u.append(("sk_comm.cpp", "sk_comm.o", []))
     return [(src, obj.replace(".o", OBJ_SUFFIX + ".o"), defs + EXTRA_DEFS) for src, obj, defs in u]
@@ -71,7 +72,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         for lg in logs:
             sys.stderr.write(lg)
     objs = [os.path.join(CSRC, u[1]) for u in us]
-    subprocess.check_call([NVCC, "-shared", *ARCH, *objs, "-o", LIB + ".tmp", "-lcudart",
+    subprocess.check_call([NVCC, "-shared", *ARCH, *objs, "-o", LIB + ".tmp", "-lcudart", "-lcublas", "-lcusolver",
                            "-Xcompiler", "-pthread", "-ldl"])
     os.replace(LIB + ".tmp", LIB)
     return LIB

@@ -162,6 +162,16 @@ struct SolveConst {
   DevState* st;
 };
 
+// operator description for the true-residual kernels (sk_residual.cu)
+struct TrOp {
+  int32_t sdim;  // 0: CSR, 2 / 3: matrix-free grid stencil
+  int64_t g;
+  double c[7];
+  const int32_t* rp;
+  const int32_t* ci;
+  const double* val;
+};
+
 __host__ __device__ __forceinline__ int64_t mn64(int64_t a, int64_t b) { return a < b ? a : b; }
 __host__ __device__ __forceinline__ int64_t mx64(int64_t a, int64_t b) { return a > b ? a : b; }
 

@@ -10,6 +10,9 @@
 #include "sk_launch.h"
 #include "sk_comm.h"
 
+#include <cublas_v2.h>
+#include <cusolverDn.h>
+
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
@@ -353,6 +356,7 @@ void h2d_staged(void* dst, const void* src, size_t bytes, cudaStream_t st) {
 
 struct DevCsr {
   int64_t n = 0, nnz = 0;
+  int64_t bw = 0;  // bandwidth max |col - row| (true residual halo)
   StencilInfo stencil;
   int32_t* rp = nullptr;
   int32_t* ci = nullptr;
@@ -373,6 +377,18 @@ size_t upload_csr(DevCsr& d, int64_t n, int64_t nnz, const int64_t* rp, const in
     d.stencil = *pre;
   else if (detect && !getenv("SK_NO_STENCIL"))
     detect_stencil(rp, ci, val, n, d.stencil);
+  if (d.stencil.dim) {
+    d.bw = d.stencil.dim == 2 ? d.stencil.g : d.stencil.g * d.stencil.g;
+  } else {
+    std::mutex mu;
+    par_rows(n, [&](int64_t lo, int64_t hi) {
+      int64_t h = 0;
+      for (int64_t i = lo; i < hi; ++i)
+        for (int64_t k = rp[i]; k < rp[i + 1]; ++k) h = std::max<int64_t>(h, std::llabs(ci[k] - i));
+      std::lock_guard<std::mutex> g(mu);
+      d.bw = std::max(d.bw, h);
+    });
+  }
   if (d.stencil.dim && !keep_csr) return 0;
   std::vector<int32_t> rp32(n + 1), ci32(std::max<int64_t>(nnz, 1));
   par_rows(n + 1, [&](int64_t lo, int64_t hi) {
@@ -1606,6 +1622,7 @@ sk_problem* create_problem(int32_t method, const sk_csr* a, const sk_csr* b, con
       p->op[1].n = b->n_cols;
       p->op[1].nnz = b->nnz;
       p->op[1].stencil = bt_st;
+      p->op[1].bw = bt_st.dim == 2 ? bt_st.g : bt_st.g * bt_st.g;
     } else if (bt_is_b ? ab_same : same_csr(a, bt)) {
       p->op[1] = p->op[0];  // e.g. A = B symmetric: B^T == A bitwise
       p->op_shared = true;
@@ -1669,9 +1686,322 @@ sk_status one_shot(int32_t method, const sk_csr* a, const sk_csr* b, const doubl
   return rc;
 }
 
+// ---------------------------------------------------------------------------
+// Device true residual (true_residual / true_residual_factors,
+// factorized_solvers.cpp:391-444). ||[C1, -A Vc, -Vc] [C2, W, B^T W]^T||_F with
+// Vc = V core, through the R factors of the two stacked factor matrices; the
+// stacked matrices are streamed in row chunks (with an operator halo) through a
+// TSQR: R <- qr([R; chunk]) (cuSOLVER geqrf on (wdt + rows) x wdt). Vc rows come
+// from one cuBLAS GEMM per chunk against the normalised basis rows. The
+// denominator ||C1 C2^T||_F is sqrt(<C1^T C1, C2^T C2>) (a positive sum).
+// ---------------------------------------------------------------------------
+struct TrBasis {
+  const double* const* blocks = nullptr;  // device table of raw blocks (normalised on gather)
+  const double* nfac = nullptr;
+  int nblk = 0, s = 0;
+  const double* dense = nullptr;          // or a column-major n x cols device matrix
+  int cols = 0;                           // basis columns
+};
+struct TrSide {
+  int64_t n = 0;
+  const double* C = nullptr;  // device, column-major n x s
+  int s = 0;
+  TrBasis basis;
+  const double* core = nullptr;  // U side: basis cols x r (column-major, ld ldcore); V side: none
+  int64_t ldcore = 0;
+  int r = 0;
+  sk::TrOp op{};
+  int64_t bw = 0;
+  bool u_side = true;  // U: [C, -op(Z), -Z], V: [C, Z, op(Z)]
+};
+
+sk::TrOp tr_op(const DevCsr& d) {
+  sk::TrOp o{};
+  o.sdim = d.stencil.dim;
+  o.g = d.stencil.g;
+  for (int q = 0; q < 7; ++q) o.c[q] = d.stencil.c[q];
+  o.rp = d.rp;
+  o.ci = d.ci;
+  o.val = d.val;
+  return o;
+}
+
+struct TrHandles {
+  cublasHandle_t cb = nullptr;
+  cusolverDnHandle_t cs = nullptr;
+  explicit TrHandles(cudaStream_t st) {
+    if (cublasCreate(&cb) != CUBLAS_STATUS_SUCCESS) throw SkError(SK_ERR_CUDA, "true_residual: cublasCreate failed");
+    if (cusolverDnCreate(&cs) != CUSOLVER_STATUS_SUCCESS) {
+      cublasDestroy(cb);
+      throw SkError(SK_ERR_CUDA, "true_residual: cusolverDnCreate failed");
+    }
+    cublasSetStream(cb, st);
+    cusolverDnSetStream(cs, st);
+  }
+  ~TrHandles() {
+    cusolverDnDestroy(cs);
+    cublasDestroy(cb);
+  }
+};
+#define CKB(x)                                                                        \
+  do {                                                                                \
+    if ((x) != CUBLAS_STATUS_SUCCESS) throw SkError(SK_ERR_CUDA, "cuBLAS: " #x);      \
+  } while (0)
+#define CKS(x)                                                                        \
+  do {                                                                                \
+    if ((x) != CUSOLVER_STATUS_SUCCESS) throw SkError(SK_ERR_CUDA, "cuSOLVER: " #x);  \
+  } while (0)
+
+struct DevBuf {
+  std::vector<void*> ptrs;
+  template <class T>
+  T* get(size_t count) {
+    void* p = nullptr;
+    CK(cudaMalloc(&p, sizeof(T) * std::max<size_t>(count, 1)));
+    ptrs.push_back(p);
+    return static_cast<T*>(p);
+  }
+  ~DevBuf() {
+    for (void* p : ptrs) cudaFree(p);
+  }
+};
+
+// R factor (wdt x wdt, upper, device column-major) of one side's stacked matrix
+void tr_side_r(const TrSide& in, int wdt, double* R, cudaStream_t st, TrHandles& h) {
+  const int kb = in.basis.cols, r = in.r;
+  const int64_t n = in.n, halo = std::min<int64_t>(in.bw, n);
+  size_t fr = 0, tot = 0;
+  CK(cudaMemGetInfo(&fr, &tot));
+  const double budget = std::min<double>((double)fr / 3.0, 8.0e9);
+  const double per_row = 8.0 * (kb + (in.core ? r : 0) + r + wdt);
+  int64_t rc = (int64_t)(budget / per_row) - 2 * halo;
+  rc = std::max<int64_t>(rc, 256);
+  if (const char* e = getenv("SK_TR_CHUNK")) rc = std::max<int64_t>(1, std::atoll(e));  // tests: force several chunks
+  rc = std::min<int64_t>(rc, n);
+  const int64_t ldm = wdt + rc;
+  DevBuf mem;
+  double* G = mem.get<double>((size_t)(rc + 2 * halo) * kb);
+  double* Z = in.core ? mem.get<double>((size_t)(rc + 2 * halo) * r) : G;
+  double* Pop = mem.get<double>((size_t)rc * r);
+  double* M = mem.get<double>((size_t)ldm * wdt);
+  double* tau = mem.get<double>(wdt);
+  int* info = mem.get<int>(1);
+  int lwork = 0;
+  CKS(cusolverDnDgeqrf_bufferSize(h.cs, (int)ldm, wdt, M, (int)ldm, &lwork));
+  double* work = mem.get<double>((size_t)lwork);
+  CK(cudaMemsetAsync(M, 0, sizeof(double) * ldm * wdt, st));
+  const double one = 1.0, zero = 0.0;
+  for (int64_t r0 = 0; r0 < n; r0 += rc) {
+    const int64_t rows = std::min<int64_t>(rc, n - r0), ext = rows + 2 * halo;
+    if (in.basis.blocks)
+      sk::launch_tr_gather_blocks(in.basis.blocks, in.basis.nfac, in.basis.s, in.basis.nblk, n, r0 - halo, ext, G, st);
+    else
+      sk::launch_tr_gather_dense(in.basis.dense, n, kb, r0 - halo, ext, G, st);
+    if (in.core)  // Z^T (r x ext) = core^T (r x kb) G^T (kb x ext): Z row-major ext x r
+      CKB(cublasDgemm(h.cb, CUBLAS_OP_T, CUBLAS_OP_N, r, (int)ext, kb, &one, in.core, (int)in.ldcore, G, kb, &zero,
+                      Z, r));
+    sk::launch_tr_apply(in.op, Z, halo, r0, rows, r, Pop, st);
+    if (in.u_side)
+      sk::launch_tr_fill(M, ldm, wdt, rows, in.C, n, in.s, r0, Pop, 0, Z, halo, r, -1.0, st);
+    else
+      sk::launch_tr_fill(M, ldm, wdt, rows, in.C, n, in.s, r0, Z, halo, Pop, 0, r, 1.0, st);
+    CKS(cusolverDnDgeqrf(h.cs, (int)(wdt + rows), wdt, M, (int)ldm, tau, work, lwork, info));
+    sk::launch_tr_keep_r(M, ldm, wdt, st);
+  }
+  CK(cudaMemcpy2DAsync(R, sizeof(double) * wdt, M, sizeof(double) * ldm, sizeof(double) * wdt, wdt,
+                       cudaMemcpyDeviceToDevice, st));
+  int hinfo = 0;
+  CK(cudaMemcpyAsync(&hinfo, info, sizeof(int), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  if (hinfo != 0) throw SkError(SK_ERR_CUDA, "true_residual: geqrf reported an illegal argument");
+}
+
+double tr_compute(const TrSide& U, const TrSide& V, cudaStream_t st) {
+  if (U.r != V.r || U.s != V.s) throw SkError(SK_ERR_DIMENSION, "true_residual: factor shapes do not conform");
+  TrHandles h(st);
+  const int s = U.s, r = U.r, wdt = s + 2 * r;
+  DevBuf mem;
+  // denominator: ||C1 C2^T||_F^2 = <C1^T C1, C2^T C2>
+  double* g12 = mem.get<double>(2 * s * s);
+  const double one = 1.0, zero = 0.0;
+  CKB(cublasDgemm(h.cb, CUBLAS_OP_T, CUBLAS_OP_N, s, s, (int)U.n, &one, U.C, (int)U.n, U.C, (int)U.n, &zero, g12, s));
+  CKB(cublasDgemm(h.cb, CUBLAS_OP_T, CUBLAS_OP_N, s, s, (int)V.n, &one, V.C, (int)V.n, V.C, (int)V.n, &zero,
+                  g12 + s * s, s));
+  std::vector<double> hg(2 * s * s);
+  CK(cudaMemcpyAsync(hg.data(), g12, sizeof(double) * 2 * s * s, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  double den2 = 0.0;
+  for (int e = 0; e < s * s; ++e) den2 += hg[e] * hg[s * s + e];
+  if (!(den2 > 0.0)) throw SkError(SK_ERR_INVALID_MATRIX, "true_residual: zero right-hand side");
+  double* RU = mem.get<double>((size_t)wdt * wdt);
+  double* RV = mem.get<double>((size_t)wdt * wdt);
+  double* RR = mem.get<double>((size_t)wdt * wdt);
+  tr_side_r(U, wdt, RU, st, h);
+  tr_side_r(V, wdt, RV, st, h);
+  CKB(cublasDgemm(h.cb, CUBLAS_OP_N, CUBLAS_OP_T, wdt, wdt, wdt, &one, RU, wdt, RV, wdt, &zero, RR, wdt));
+  std::vector<double> hr((size_t)wdt * wdt);
+  CK(cudaMemcpyAsync(hr.data(), RR, sizeof(double) * wdt * wdt, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  double num2 = 0.0;
+  for (double v : hr) num2 += v * v;
+  return std::sqrt(num2) / std::sqrt(den2);
+}
+
+// operators and right-hand sides of a residual evaluation on the device
+struct TrInputs {
+  DevCsr op[2];
+  bool shared = false;
+  double* c1 = nullptr;
+  double* c2 = nullptr;
+  int64_t n = 0, m = 0, s = 0;
+  ~TrInputs() {
+    free_csr(op[0]);
+    if (!shared) free_csr(op[1]);
+    cudaFree(c1);
+    cudaFree(c2);
+  }
+};
+// true_residual_factors shape checks (factorized_solvers.cpp:394-400)
+void tr_check(const sk_csr* a, const sk_csr* b, int64_t s, int64_t n_v, int64_t rv, int64_t core_r,
+              int64_t core_c, int64_t m_w, int64_t rw) {
+  validate_csr(a, "A");
+  validate_csr(b, "B");
+  if (a->n_rows != a->n_cols || b->n_rows != b->n_cols)
+    throw SkError(SK_ERR_DIMENSION, "true_residual: A and B must be square");
+  if (s < 1) throw SkError(SK_ERR_DIMENSION, "true_residual: right-hand side shapes do not conform");
+  if (n_v != a->n_rows || m_w != b->n_rows || rv != core_r || rw != core_c)
+    throw SkError(SK_ERR_DIMENSION, "true_residual: factor shapes do not conform");
+  if (a->n_rows >= (int64_t(1) << 31) || b->n_rows >= (int64_t(1) << 31) || s + 2 * rw >= 46341)
+    throw SkError(SK_ERR_UNSUPPORTED, "true_residual: sizes beyond the device path's int32 limits");
+}
+void tr_upload(TrInputs& in, const sk_csr* a, const sk_csr* b, const double* c1, const double* c2, int64_t s,
+               cudaStream_t st) {
+  in.n = a->n_rows;
+  in.m = b->n_rows;
+  in.s = s;
+  upload_csr(in.op[0], a->n_rows, a->nnz, a->row_ptr, a->col_idx, a->values, st);
+  StencilInfo sb;
+  const bool use_st = !getenv("SK_NO_STENCIL");
+  if (use_st) detect_stencil(b->row_ptr, b->col_idx, b->values, b->n_rows, sb);
+  if (same_csr(a, b) && (stencil_symmetric(sb) || bitwise_symmetric(b))) {
+    in.op[1] = in.op[0];
+    in.shared = true;
+  } else if (sb.dim) {  // B^T of a stencil: mirrored coefficients
+    const int ns = sb.dim == 2 ? 5 : 7;
+    StencilInfo t = sb;
+    for (int q = 0; q < ns; ++q) t.c[q] = sb.c[ns - 1 - q];
+    in.op[1].n = b->n_rows;
+    in.op[1].nnz = b->nnz;
+    in.op[1].stencil = t;
+    in.op[1].bw = sb.dim == 2 ? sb.g : sb.g * sb.g;
+  } else {
+    HostCsr t = transpose(b);
+    upload_csr(in.op[1], t.n_rows, (int64_t)t.val.size(), t.rp.data(), t.ci.data(), t.val.data(), st, false);
+  }
+  CK(cudaMalloc(&in.c1, sizeof(double) * in.n * s));
+  CK(cudaMalloc(&in.c2, sizeof(double) * in.m * s));
+  h2d_staged(in.c1, c1, sizeof(double) * in.n * s, st);
+  h2d_staged(in.c2, c2, sizeof(double) * in.m * s, st);
+}
+TrSide tr_side(const DevCsr& op, const double* C, int64_t n, int64_t s, bool u_side) {
+  TrSide t;
+  t.n = n;
+  t.C = C;
+  t.s = (int)s;
+  t.op = tr_op(op);
+  t.bw = op.bw;
+  t.u_side = u_side;
+  return t;
+}
+// residual of a device-resident solution against device operators / RHS
+double tr_solution(const DevCsr& opa, const DevCsr& opbt, const double* c1, const double* c2, int64_t s,
+                   const sk_solution* sol, cudaStream_t st) {
+  if (sol->row0_v != 0 || sol->row0_w != 0 || (sol->rv > 0 && sol->vblocks.empty()))
+    throw SkError(SK_ERR_UNSUPPORTED, "true_residual: row-partitioned solutions are not supported");
+  if (sol->rv == 0 || sol->rw == 0) throw SkError(SK_ERR_DIMENSION, "true_residual: empty solution");
+  DevBuf mem;
+  const int bs = (int)sol->s;
+  const int nbv = (int)(sol->rv / bs), nbw = (int)(sol->rw / bs);
+  const double** tv = mem.get<const double*>(nbv);
+  const double** tw = mem.get<const double*>(nbw);
+  CK(cudaMemcpyAsync(tv, sol->vblocks.data(), sizeof(double*) * nbv, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(tw, sol->wblocks.data(), sizeof(double*) * nbw, cudaMemcpyHostToDevice, st));
+  TrSide U = tr_side(opa, c1, sol->n, s, true), V = tr_side(opbt, c2, sol->m, s, false);
+  U.basis = {tv, sol->vnfac, nbv, bs, nullptr, (int)sol->rv};
+  U.core = sol->X;
+  U.ldcore = sol->ld;
+  U.r = (int)sol->rw;
+  V.basis = {tw, sol->wnfac, nbw, bs, nullptr, (int)sol->rw};
+  V.r = (int)sol->rw;
+  return tr_compute(U, V, st);
+}
+
 }  // namespace
 
 extern "C" {
+
+sk_status sk_true_residual(const sk_csr* a, const sk_csr* b, const double* c1, const double* c2, int64_t s,
+                           const sk_solution* sol, double* rel) {
+  return run_guarded([&] {
+    if (!sol || !rel || !c1 || !c2) throw SkError(SK_ERR_DIMENSION, "true_residual: null argument");
+    tr_check(a, b, s, sol->n, sol->rv, sol->rv, sol->rw, sol->m, sol->rw);
+    CK(cudaSetDevice(sol->device));
+    cudaStream_t st;
+    CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    struct SG {
+      cudaStream_t s;
+      ~SG() { cudaStreamDestroy(s); }
+    } sg{st};
+    TrInputs in;
+    tr_upload(in, a, b, c1, c2, s, st);
+    *rel = tr_solution(in.op[0], in.op[1], in.c1, in.c2, s, sol, st);
+  });
+}
+
+sk_status sk_true_residual_factors(const sk_csr* a, const sk_csr* b, const double* c1, const double* c2, int64_t s,
+                                   const double* v, int64_t rv, const double* core, const double* w, int64_t rw,
+                                   double* rel) {
+  return run_guarded([&] {
+    if (!rel || !c1 || !c2 || !v || !core || !w) throw SkError(SK_ERR_DIMENSION, "true_residual: null argument");
+    tr_check(a, b, s, a->n_rows, rv, rv, rw, b->n_rows, rw);
+    check_device(0);
+    cudaStream_t st;
+    CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    struct SG {
+      cudaStream_t s;
+      ~SG() { cudaStreamDestroy(s); }
+    } sg{st};
+    TrInputs in;
+    tr_upload(in, a, b, c1, c2, s, st);
+    DevBuf mem;
+    double* dv = mem.get<double>((size_t)in.n * rv);
+    double* dc = mem.get<double>((size_t)rv * rw);
+    double* dw = mem.get<double>((size_t)in.m * rw);
+    h2d_staged(dv, v, sizeof(double) * in.n * rv, st);
+    h2d_staged(dc, core, sizeof(double) * rv * rw, st);
+    h2d_staged(dw, w, sizeof(double) * in.m * rw, st);
+    TrSide U = tr_side(in.op[0], in.c1, in.n, s, true), V = tr_side(in.op[1], in.c2, in.m, s, false);
+    U.basis.dense = dv;
+    U.basis.cols = (int)rv;
+    U.core = dc;
+    U.ldcore = rv;
+    U.r = (int)rw;
+    V.basis.dense = dw;
+    V.basis.cols = (int)rw;
+    V.r = (int)rw;
+    *rel = tr_compute(U, V, st);
+  });
+}
+
+sk_status sk_problem_true_residual(const sk_problem* p, const sk_solution* sol, double* rel) {
+  return run_guarded([&] {
+    if (!p || !sol || !rel) throw SkError(SK_ERR_DIMENSION, "true_residual: null argument");
+    if (p->world > 1) throw SkError(SK_ERR_UNSUPPORTED, "true_residual: row-partitioned problems are not supported");
+    CK(cudaSetDevice(p->device));
+    const bool lyap = p->method == SK_METHOD_CG_LYAPUNOV;
+    *rel = tr_solution(p->op[0], lyap ? p->op[0] : p->op[1], p->c1, lyap ? p->c1 : p->c2, p->s, sol, p->stream);
+  });
+}
 
 sk_status sk_factorized_cg(const sk_csr* a, const sk_csr* b, const double* c1, const double* c2,
                            int64_t s, const sk_config* cfg, const sk_gpu_options* gpu,

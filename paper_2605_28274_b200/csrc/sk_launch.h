@@ -36,4 +36,15 @@ void launch_gram_loop(const SolveConst& c, cudaStream_t st);
 void launch_update_clean(const SolveConst& c, cudaStream_t st);
 void launch_block_to_colmajor(const double* blk, double* out, int64_t n, int s, cudaStream_t st);
 void launch_colmajor_to_block(const double* in, double* blk, int64_t n, int s, cudaStream_t st);
+// device true residual (sk_residual.cu)
+struct TrOp;
+void launch_tr_gather_blocks(const double* const* blocks, const double* nfac, int s, int nblk, int64_t n, int64_t r0,
+                             int64_t rows, double* G, cudaStream_t st);
+void launch_tr_gather_dense(const double* X, int64_t n, int cols, int64_t r0, int64_t rows, double* G,
+                            cudaStream_t st);
+void launch_tr_apply(const TrOp& op, const double* X, int64_t h, int64_t r0, int64_t rows, int r, double* Y,
+                     cudaStream_t st);
+void launch_tr_fill(double* M, int64_t ldm, int64_t off, int64_t rows, const double* C, int64_t n, int s, int64_t r0,
+                    const double* P1, int64_t h1, const double* P2, int64_t h2, int r, double sgn, cudaStream_t st);
+void launch_tr_keep_r(double* M, int64_t ldm, int wdt, cudaStream_t st);
 }  // namespace sk

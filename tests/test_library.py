@@ -133,3 +133,14 @@ def test_symmetry_checks(skl):
     s = _csr_from_dense(skl, sym)
     with pytest.raises(skl.InvalidMatrixError, match="B is not symmetric"):
         skl.factorized_cg(s, a, np.ones((40, 1)), np.ones((40, 1)))
+
+
+def test_true_residual_shape_checks_before_device(skl):
+    """true_residual_factors shape checks (factorized_solvers.cpp:394-400) run on the host."""
+    a = skl.SparseMatrix.identity(4)
+    with pytest.raises(skl.DimensionError):
+        skl.true_residual_factors(a, a, np.ones((4, 1)), np.ones((4, 1)), np.ones((4, 2)), np.ones((3, 2)),
+                                  np.ones((4, 2)))
+    with pytest.raises(skl.DimensionError):
+        skl.true_residual_factors(a, a, np.ones((4, 1)), np.ones((4, 2)), np.ones((4, 2)), np.ones((2, 2)),
+                                  np.ones((4, 2)))
