@@ -250,10 +250,14 @@ __device__ inline bool cholesky_upper(const double* G, int s, double* R) {
   }
   return true;
 }
-// One-sided Jacobi singular-value extremes (oracle: jacobi_extremes).
+// One-sided Jacobi singular-value extremes (oracle: jacobi_extremes). Called by
+// one thread of a CTA; the work arrays live in shared memory (a runtime-indexed
+// local array would go to local memory, i.e. an L2 round trip per access while
+// the rest of the GPU waits on this serial finalisation).
 __device__ inline void jacobi_extremes(const double* m, int rows, int cols, double* smax,
                                        double* smin) {
-  double A[kMaxS * kMaxS];
+  __shared__ double A[kMaxS * kMaxS];
+  __shared__ double nv[kMaxS];
   for (int e = 0; e < rows * cols; ++e) A[e] = m[e];
   for (int sweep = 0; sweep < 60; ++sweep) {
     bool rotated = false;
@@ -287,7 +291,6 @@ __device__ inline void jacobi_extremes(const double* m, int rows, int cols, doub
     if (!rotated) break;
   }
   const int k = rows < cols ? rows : cols;
-  double nv[kMaxS];
   for (int j = 0; j < cols; ++j) {
     double acc = 0.0;
     for (int i = 0; i < rows; ++i) acc = __dadd_rn(acc, __dmul_rn(A[j * rows + i], A[j * rows + i]));

@@ -23,6 +23,7 @@
 #include "sk_launch.h"
 
 #include <cstdlib>
+#include <cstdio>
 
 namespace sk {
 
@@ -83,7 +84,8 @@ __device__ inline double* hcol_ptr(const SideConst& sc, int64_t e, int cc, int s
 
 // coeff2 (block_krylov.cpp:105-108): Lanczos in the reference loop order; Arnoldi
 // as the canonical tree over per-block sums hsq[b] (written by the Gram pass).
-__device__ inline double coeff2_of(const SolveConst& c, int side, int64_t k, int64_t e) {
+// cc (optional): shared-memory copy of the coefficient blocks k-2, k-1 (s*s each)
+__device__ inline double coeff2_of(const SolveConst& c, int side, int64_t k, int64_t e, const double* cc) {
   const SideConst& sc = c.side[side];
   const int s = c.s, ss = s * s;
   if (c.arnoldi) {
@@ -94,9 +96,9 @@ __device__ inline double coeff2_of(const SolveConst& c, int side, int64_t k, int
   }
   double acc = 0.0;
   for (int64_t jb = first_block(c, k); jb < k; ++jb)
-    for (int cc = 0; cc < s; ++cc)
+    for (int col = 0; col < s; ++col)
       for (int r = 0; r < s; ++r) {
-        const double h = __ldcg(sc.coef + jb * ss + cc * s + r);
+        const double h = cc ? cc[(jb - (k - 2)) * ss + col * s + r] : __ldcg(sc.coef + jb * ss + col * s + r);
         acc = __dadd_rn(acc, __dmul_rn(h, h));
       }
   (void)e;
@@ -134,7 +136,7 @@ static __device__ double block_tree(const double* a, int64_t count, double* sbuf
 __device__ inline void set_nfac(const SideConst& sc, int64_t b, int s, const double* N, bool identity) {
   double* p = sc.nfac + b * (s * s + s);
   for (int e = 0; e < s * s; ++e) p[e] = identity ? ((e % (s + 1)) == 0 ? 1.0 : 0.0) : N[e];
-  for (int u = 0; u < s; ++u) p[s * s + u] = __ddiv_rn(1.0, p[u * s + u]);
+  for (int u = 0; u < s; ++u) p[s * s + u] = __ddiv_rn(1.0, identity ? 1.0 : N[u * s + u]);
 }
 
 // c = N^{-T} G and M = N^{-1} c (oracle tri_ntinv / tri_ninv), N with 1/diag in nfac
@@ -155,9 +157,8 @@ __device__ inline void block_coefs(const double* nf, const double* G, int s, dou
     }
 }
 
-__device__ inline void commit_grow(const SolveConst& c, int side, int grow_stage) {
+__device__ inline void commit_grow(const SolveConst& c, int side, int grow_stage, SideState& st, const double* cc) {
   const SideConst& sc = c.side[side];
-  SideState& st = c.st->side[side];
   const int s = c.s, ss = s * s;
   const int64_t k = st.blocks, e = st.steps;
   if (!c.arnoldi) {
@@ -165,8 +166,8 @@ __device__ inline void commit_grow(const SolveConst& c, int side, int grow_stage
     double* h1 = hb_ptr(sc, e, 1, s);
     double* h2 = hb_ptr(sc, e, 2, s);
     for (int x = 0; x < ss; ++x) {
-      h0[x] = (k >= 2) ? __ldcg(sc.coef + (k - 2) * ss + x) : 0.0;
-      h1[x] = __ldcg(sc.coef + (k - 1) * ss + x);
+      h0[x] = (k >= 2) ? (cc ? cc[x] : __ldcg(sc.coef + (k - 2) * ss + x)) : 0.0;
+      h1[x] = cc ? cc[ss + x] : __ldcg(sc.coef + (k - 1) * ss + x);
       h2[x] = st.R[x];
     }
   } else {
@@ -179,9 +180,8 @@ __device__ inline void commit_grow(const SolveConst& c, int side, int grow_stage
   st.blocks = k + 1;
   st.stage = grow_stage;
 }
-__device__ inline void commit_exhausted(const SolveConst& c, int side) {
+__device__ inline void commit_exhausted(const SolveConst& c, int side, SideState& st, const double* cc) {
   const SideConst& sc = c.side[side];
-  SideState& st = c.st->side[side];
   const int s = c.s, ss = s * s;
   const int64_t k = st.blocks, e = st.steps;
   if (!c.arnoldi) {
@@ -189,8 +189,8 @@ __device__ inline void commit_exhausted(const SolveConst& c, int side) {
     double* h1 = hb_ptr(sc, e, 1, s);
     double* h2 = hb_ptr(sc, e, 2, s);
     for (int x = 0; x < ss; ++x) {
-      h0[x] = (k >= 2) ? __ldcg(sc.coef + (k - 2) * ss + x) : 0.0;
-      h1[x] = __ldcg(sc.coef + (k - 1) * ss + x);
+      h0[x] = (k >= 2) ? (cc ? cc[x] : __ldcg(sc.coef + (k - 2) * ss + x)) : 0.0;
+      h1[x] = cc ? cc[ss + x] : __ldcg(sc.coef + (k - 1) * ss + x);
       h2[x] = 0.0;
     }
   } else {
@@ -204,11 +204,11 @@ __device__ inline void commit_exhausted(const SolveConst& c, int side) {
 }
 
 // classification (block_krylov.cpp:105-137)
-__device__ inline void classify(const SolveConst& c, int side, bool first_pass, int grow_stage) {
-  SideState& st = c.st->side[side];
+__device__ inline void classify(const SolveConst& c, int side, bool first_pass, int grow_stage, SideState& st,
+                                const double* cc = nullptr) {
   const int s = c.s, ss = s * s;
   if (first_pass) {
-    if (!(c.arnoldi && st.pad == 1)) st.coeff2 = coeff2_of(c, side, st.blocks, st.steps);
+    if (!(c.arnoldi && st.pad == 1)) st.coeff2 = coeff2_of(c, side, st.blocks, st.steps, cc);
     st.pad = 0;
     double r2 = 0.0;
     for (int x = 0; x < ss; ++x) r2 = __dadd_rn(r2, __dmul_rn(st.R[x], st.R[x]));
@@ -221,7 +221,7 @@ __device__ inline void classify(const SolveConst& c, int side, bool first_pass, 
   }
   const double lim = __dmul_rn(c.tol, st.scale);
   if (st.smax <= lim || st.scale == 0.0) {
-    commit_exhausted(c, side);
+    commit_exhausted(c, side, st, cc);
     return;
   }
   if (st.smin < lim) {
@@ -229,27 +229,39 @@ __device__ inline void classify(const SolveConst& c, int side, bool first_pass, 
     st.stage = ST_DONE_NOGROW;
     return;
   }
-  commit_grow(c, side, grow_stage);
+  commit_grow(c, side, grow_stage, st, cc);
 }
 
 // after the direct Gram (gbase) of the candidate in U_k
-__device__ inline void finalize_direct(const SolveConst& c, int side, bool first_pass) {
-  SideState& st = c.st->side[side];
+#ifdef SK_CS_PROF
+__device__ long long g_fdprof[4];
+#endif
+__device__ inline void finalize_direct(const SolveConst& c, int side, bool first_pass, SideState& st,
+                                       const double* cc = nullptr) {
   const int s = c.s;
+#ifdef SK_CS_PROF
+  const long long f0 = clock64();
+#endif
   bool ok = cholesky_upper(st.gbase, s, st.R);
+#ifdef SK_CS_PROF
+  const long long f1 = clock64();
+#endif
   if (ok) {
     jacobi_extremes(st.R, s, s, &st.smax, &st.smin);
     if (st.smin < __dmul_rn(kHHRatio, st.smax)) ok = false;
   }
+#ifdef SK_CS_PROF
+  g_fdprof[0] = f1 - f0;
+  g_fdprof[1] = clock64() - f1;
+#endif
   if (!ok) {
     st.stage = first_pass ? ST_NEED_HH : ST_NEED_HH2;
     return;
   }
   if (first_pass) st.paths[0]++;
-  classify(c, side, first_pass, ST_GROW_DIRECT);
+  classify(c, side, first_pass, ST_GROW_DIRECT, st, cc);
 }
-__device__ inline void finalize_init(const SolveConst& c, int side) {
-  SideState& st = c.st->side[side];
+__device__ inline void finalize_init(const SolveConst& c, int side, SideState& st) {
   const int s = c.s;
   bool ok = cholesky_upper(st.gbase, s, st.R);
   if (ok) {
@@ -864,13 +876,26 @@ __device__ __forceinline__ void p1_dispatch(const SideConst& sc, const double* _
 // of Gamma normalised like a basis row) -> c_b, M_b for blocks k-2 (if any), k-1
 template <int S>
 __device__ __noinline__ void p1_finish(const SideConst& sc, int64_t k, const double* res) {
-  constexpr int NB = S * S;
+  constexpr int NB = S * S, NF1 = S * S + S;
+  // factors of blocks k-2, k-1 staged by all threads (block k-1's was just
+  // committed by this CTA's finalisation), then two threads finish the slots
+  __shared__ double nfs[2 * NF1];
+#ifdef SK_CS_PROF
+  const long long pp0 = clock64();
+#endif
+  __syncthreads();
+  for (int i = threadIdx.x; i < 2 * NF1; i += blockDim.x) {
+    const int64_t b = k - 2 + i / NF1;
+    nfs[i] = b >= 0 ? sc.nfac[b * NF1 + i % NF1] : 0.0;
+  }
+  __syncthreads();
   if (threadIdx.x < 2) {
     const int slot = threadIdx.x;  // 0: block k-2, 1: block k-1
     if (slot == 1 || k >= 2) {
       const int64_t b = slot == 0 ? k - 2 : k - 1;
       NF<S> fk;
-      load_nf<S>(sc.nfac, k - 1, fk);
+      for (int e = 0; e < NB; ++e) fk.N[e] = nfs[NF1 + e];
+      for (int u = 0; u < S; ++u) fk.d[u] = nfs[NF1 + NB + u];
       double G[NB];
       for (int t = 0; t < S; ++t) {
         double row[S], q[S];
@@ -879,19 +904,42 @@ __device__ __noinline__ void p1_finish(const SideConst& sc, int64_t k, const dou
         for (int u = 0; u < S; ++u) G[u * S + t] = q[u];
       }
       double cb[NB], mb[NB];
-      block_coefs(sc.nfac + b * (NB + S), G, S, cb, mb);
+      block_coefs(nfs + slot * NF1, G, S, cb, mb);
       for (int e = 0; e < NB; ++e) {
         sc.coef[b * NB + e] = cb[e];
         sc.mcoef[b * NB + e] = mb[e];
       }
     }
   }
+#ifdef SK_CS_PROF
+  __syncthreads();
+  if (threadIdx.x == 0 && (k == 101 || k == 151)) printf("P1FIN %lld cyc\n", clock64() - pp0);
+#endif
 }
-// self-Gram root -> gbase (symmetric), then finalisation
+// self-Gram root -> gbase (symmetric), then finalisation. The finalisation is a
+// single-thread chain of small dependent steps (Cholesky, Jacobi, classification,
+// commit); it runs on a shared-memory copy of the side state, so the chain sees
+// shared-memory latency instead of a global round trip per access.
 template <int S>
 __device__ __noinline__ void gram_finish(const SolveConst& c, int side, const double* res, int how) {
   constexpr int NS = S * (S + 1) / 2;
-  SideState& sst = c.st->side[side];
+  constexpr int NW = (int)(sizeof(SideState) / sizeof(unsigned long long));
+  static_assert(sizeof(SideState) % sizeof(unsigned long long) == 0, "SideState is word-sized");
+  __shared__ SideState sst;
+  unsigned long long* gw = reinterpret_cast<unsigned long long*>(&c.st->side[side]);
+  unsigned long long* sw = reinterpret_cast<unsigned long long*>(&sst);
+  __shared__ double ccache[2 * S * S];  // coefficient blocks k-2, k-1 (Lanczos)
+  for (int i = threadIdx.x; i < NW; i += blockDim.x) sw[i] = __ldcg(gw + i);
+  {
+    const int64_t k = c.st->side[side].blocks;
+    const SideConst& sc = c.side[side];
+    for (int i = threadIdx.x; i < 2 * S * S; i += blockDim.x) {
+      const int64_t b = k - 2 + i / (S * S);
+      ccache[i] = (b >= 0 && !c.arnoldi) ? __ldcg(sc.coef + b * S * S + i % (S * S)) : 0.0;
+    }
+  }
+  __syncthreads();
+  const double* cc = c.arnoldi ? nullptr : ccache;
   for (int e = threadIdx.x; e < NS; e += blockDim.x) {
     int t, u;
     unpack_tri(e, t, u);
@@ -899,16 +947,31 @@ __device__ __noinline__ void gram_finish(const SolveConst& c, int side, const do
     sst.gbase[t * S + u] = res[e];
   }
   __syncthreads();
+#ifdef SK_CS_PROF
+  long long pq0 = clock64();
+#endif
   if (threadIdx.x == 0) {
     if (how == 2) {
-      finalize_init(c, side);
+      finalize_init(c, side, sst);
     } else if (how == 1) {
       sst.paths[2]++;
-      finalize_direct(c, side, false);
+      finalize_direct(c, side, false, sst, cc);
     } else {
-      finalize_direct(c, side, true);
+      finalize_direct(c, side, true, sst, cc);
     }
   }
+  __syncthreads();
+#ifdef SK_CS_PROF
+  long long pq1 = clock64();
+#endif
+  for (int i = threadIdx.x; i < NW; i += blockDim.x) gw[i] = sw[i];
+  __threadfence_block();
+  __syncthreads();
+#ifdef SK_CS_PROF
+  if (threadIdx.x == 0 && (sst.blocks == 101 || sst.blocks == 151))
+    printf("GFIN side %d chain %lld cyc, copyout %lld cyc (chol %lld jacobi %lld)\n", side, pq1 - pq0, clock64() - pq1,
+           g_fdprof[0], g_fdprof[1]);
+#endif
 }
 
 // Lanczos pass 1: w = (op U_{k-1}) N_{k-1}^{-1}; G = U_{k-2}^T w, U_{k-1}^T w
@@ -1244,7 +1307,8 @@ constexpr int kCsK = kSeg + 2;             // U_k / U_{k-2} lines: columns x0-1 
 constexpr int kCsAR = 8;                   // U_{k-1} ring: lines y-3 .. y+4 (prefetch 4)
 constexpr int kCsBR = 8;                   // U_{k-2} ring: lines y-3 .. y+4 (prefetch 4)
 constexpr int kCsKR = 4;                   // U_k ring: lines y-3 .. y
-constexpr int kCsMaxLines = 4096;
+constexpr int kCsMaxLines = 1024;          // lines per range (the tail's line nodes fit in the rings)
+constexpr int kCsBlk = 8;                  // lines per tail block node (range alignment)
 
 template <int S>
 __device__ __forceinline__ void cs_copy(double* dst, const double* src, bool ok) {
@@ -1275,6 +1339,50 @@ __device__ __forceinline__ void cs_stencil(const double* c5, const double* up, c
   }
 }
 
+#ifdef SK_CS_PROF
+__device__ unsigned long long g_csprof[2][1024][4];
+#endif
+// canonical tree over N values src[j * stride], j < N (N a power of two)
+template <int N>
+__device__ __forceinline__ double cs_group_tree(const double* __restrict__ src, int stride) {
+  double a[N];
+#pragma unroll
+  for (int j = 0; j < N; ++j) a[j] = __ldcg(src + (int64_t)j * stride);
+#pragma unroll
+  for (int w = N / 2; w >= 1; w >>= 1)
+#pragma unroll
+    for (int j = 0; j < w; ++j) a[j] = __dadd_rn(a[2 * j], a[2 * j + 1]);
+  return a[0];
+}
+// line nodes of a range: ln[l*NE + e] = canonical tree over the NSTRIP segment
+// partials gs[(l*NSTRIP + q)*NE + e]; four items per thread in flight
+template <int NE, int NSTRIP>
+__device__ __forceinline__ void cs_line_nodes(const double* __restrict__ gs, int nitem, double* ln) {
+  constexpr int U = 4;
+  for (int i0 = threadIdx.x; i0 < nitem; i0 += U * blockDim.x) {
+    double vv[U][NSTRIP];
+#pragma unroll
+    for (int h = 0; h < U; ++h) {
+      const int idx = i0 + h * blockDim.x;
+      if (idx < nitem) {
+        const int l = idx / NE, e = idx - l * NE;
+#pragma unroll
+        for (int q = 0; q < NSTRIP; ++q) vv[h][q] = __ldcg(gs + ((int64_t)l * NSTRIP + q) * NE + e);
+      }
+    }
+#pragma unroll
+    for (int h = 0; h < U; ++h) {
+      const int idx = i0 + h * blockDim.x;
+      if (idx < nitem) {
+#pragma unroll
+        for (int w = NSTRIP / 2; w >= 1; w >>= 1)
+#pragma unroll
+          for (int j = 0; j < w; ++j) vv[h][j] = __dadd_rn(vv[h][2 * j], vv[h][2 * j + 1]);
+        ln[idx] = vv[h][0];
+      }
+    }
+  }
+}
 template <int S>
 __global__ void __launch_bounds__(kCsThreads, 1)
     k_lanczos_cols(const __grid_constant__ SolveConst c, int side0, int nranges) {
@@ -1290,10 +1398,15 @@ __global__ void __launch_bounds__(kCsThreads, 1)
   const int g = (int)sc.sg;
   const int nstrip = g / kSeg;
   const int sx = blockIdx.x % nstrip, rg = blockIdx.x / nstrip;
-  const int y0 = (int)((int64_t)rg * g / nranges), y1 = (int)((int64_t)(rg + 1) * g / nranges);
+  // line ranges are aligned to kCsBlk lines (the tail reduces whole line blocks)
+  const int y0 = (int)((int64_t)rg * (g / kCsBlk) / nranges) * kCsBlk;
+  const int y1 = (int)((int64_t)(rg + 1) * (g / kCsBlk) / nranges) * kCsBlk;
   const int x0 = sx * kSeg;
   const int64_t k = ss.blocks;
   const bool two = k >= 2;
+#ifdef SK_CS_PROF
+  if (threadIdx.x == 0) g_csprof[blockIdx.y][blockIdx.x][0] = globaltimer();
+#endif
   extern __shared__ __align__(16) double cs_smem[];
   double* Ar = cs_smem;                    // [kCsAR][AL]
   double* Br = Ar + kCsAR * AL;            // [kCsBR][KL]
@@ -1503,19 +1616,88 @@ __global__ void __launch_bounds__(kCsThreads, 1)
   }
   asm volatile("cp.async.wait_all;" ::: "memory");
   unsigned* ctr = sc.sctr;  // [0..nranges) per range, [nranges] per side
+#ifdef SK_CS_PROF
+  if (threadIdx.x == 0) g_csprof[blockIdx.y][blockIdx.x][1] = globaltimer();
+#endif
   if (!last_cta_arrive(ctr + rg, (unsigned)nstrip)) return;
-  for (int idx = threadIdx.x; idx < (y1 - y0) * NE; idx += blockDim.x) {
-    const int l = idx / NE, e = idx - l * NE;
-    double vv[8];
-    for (int q = 0; q < nstrip; ++q) vv[q] = __ldcg(gseg + ((int64_t)(y0 + l) * nstrip + q) * NE + e);
-    lnode[(int64_t)(y0 + l) * NE + e] = tree_reduce_local(vv, nstrip);
+  // last strip CTA of the range: line nodes (canonical tree over the line's nstrip
+  // segment partials) into shared memory, then one node per aligned block of
+  // kCsBlk lines to HBM. Both are subtrees of the canonical tree over all segments.
+  {
+    double* ln = cs_smem;  // [(y1 - y0)][NE]
+    const double* gs = gseg + (int64_t)y0 * nstrip * NE;
+    const int nitem = (y1 - y0) * NE;
+    switch (nstrip) {
+      case 1: cs_line_nodes<NE, 1>(gs, nitem, ln); break;
+      case 2: cs_line_nodes<NE, 2>(gs, nitem, ln); break;
+      case 4: cs_line_nodes<NE, 4>(gs, nitem, ln); break;
+      default: cs_line_nodes<NE, 8>(gs, nitem, ln); break;
+    }
+    __syncthreads();
+    const int nb = (y1 - y0) / kCsBlk;
+    for (int idx = threadIdx.x; idx < nb * NE; idx += blockDim.x) {
+      const int b = idx / NE, e = idx - b * NE;
+      double a[kCsBlk];
+#pragma unroll
+      for (int j = 0; j < kCsBlk; ++j) a[j] = ln[(b * kCsBlk + j) * NE + e];
+      lnode[(int64_t)(y0 / kCsBlk + b) * NE + e] = tree_reduce_local(a, kCsBlk);
+    }
   }
+#ifdef SK_CS_PROF
+  __syncthreads();
+  if (threadIdx.x == 0) g_csprof[blockIdx.y][blockIdx.x][2] = globaltimer();
+#endif
   if (!last_cta_arrive(ctr + nranges, (unsigned)nranges)) return;
+  // root: canonical tree over the g / kCsBlk block nodes, one warp per entry:
+  // lane l reduces its aligned group of P/32, then pairs of lanes (xor 1, 2, .., 16)
   __shared__ double res[NE];
-  final_tree<NE>(lnode, g, res, lnode + (int64_t)g * NE);
+  if (warp < NE) {
+    const int P = g / kCsBlk, per = P / 32;  // g = 512 * 2^j: P >= 64, per = 2^j'
+    const double* src = lnode + (int64_t)lane * per * NE + warp;
+    double v;
+    switch (per) {
+      case 2: v = cs_group_tree<2>(src, NE); break;
+      case 4: v = cs_group_tree<4>(src, NE); break;
+      case 8: v = cs_group_tree<8>(src, NE); break;
+      default: v = cs_group_tree<16>(src, NE); break;
+    }
+#pragma unroll
+    for (int d = 1; d <= 16; d <<= 1) v = __dadd_rn(v, __shfl_xor_sync(0xffffffffu, v, d));
+    if (lane == 0) res[warp] = v;
+  }
+  __syncthreads();
+#ifdef SK_CS_PROF
+  __syncthreads();
+  const unsigned long long pft = globaltimer();
+#endif
   gram_finish<S>(c, side, res, 0);
   __syncthreads();
   if (st->side[side].stage == ST_GROW_DIRECT) p1_finish<S>(sc, k + 1, res + NS);
+#ifdef SK_CS_PROF
+  __syncthreads();
+  if (threadIdx.x == 0 && (k == 100 || k == 150)) {
+    const unsigned long long pend = globaltimer();
+    unsigned long long e0 = ~0ull, l0 = ~0ull, l1 = 0, n1 = 0, lsum = 0;
+    const int nc = gridDim.x;
+    for (int i = 0; i < nc; ++i) {
+      const unsigned long long* q = g_csprof[blockIdx.y][i];
+      e0 = q[0] < e0 ? q[0] : e0;
+      l0 = q[1] < l0 ? q[1] : l0;
+      l1 = q[1] > l1 ? q[1] : l1;
+      lsum += q[1];
+    }
+    for (int r = 0; r < nranges; ++r) {
+      const unsigned long long* q = g_csprof[blockIdx.y][r * nstrip];
+      for (int i = 0; i < nstrip; ++i) {
+        const unsigned long long t2 = g_csprof[blockIdx.y][r * nstrip + i][2];
+        if (t2 > n1 && t2 >= e0 && t2 < pend) n1 = t2;
+      }
+      (void)q;
+    }
+    printf("CSTAIL side %d k %lld ctas %d: loop end min %llu mean %llu max %llu | line nodes done %llu | final tree done %llu | finish done %llu (ns from entry)\n",
+           (int)blockIdx.y, (long long)k, nc, l0 - e0, lsum / nc - e0, l1 - e0, n1 - e0, pft - e0, pend - e0);
+  }
+#endif
 }
 
 // Clean-up Gram (rare path): each CTA sweeps all blocks for its row group, so
@@ -1715,7 +1897,7 @@ __global__ void __launch_bounds__(kFusedThreads) k_self_gram(const __grid_consta
       sst.pad = 1;  // coeff2 precomputed for this step
     }
   }
-  if (threadIdx.x == 0) finalize_direct(c, side, true);
+  if (threadIdx.x == 0) finalize_direct(c, side, true, c.st->side[side]);
   (void)mode;
 }
 
@@ -1973,7 +2155,7 @@ __global__ void __launch_bounds__(1024) k_householder(const __grid_constant__ So
       accept = 1;
     } else {
       if (which == 0) st.paths[1]++;
-      classify(c, side, which == 0, ST_GROW_HH);
+      classify(c, side, which == 0, ST_GROW_HH, c.st->side[side]);
       accept = st.stage == ST_GROW_HH;
     }
   }
@@ -2743,7 +2925,7 @@ struct Launch {
     r = r < 1 ? 1 : r;
     const int64_t rmin = (sc.sg + kCsMaxLines - 1) / kCsMaxLines;
     if (r < rmin) r = rmin;
-    if (r > sc.sg) r = sc.sg;
+    if (r > sc.sg / kCsBlk) r = sc.sg / kCsBlk;
     return (int)r;
   }
   static void cols_launch(const SolveConst& c, int side0, int nz, cudaStream_t st) {
