@@ -23,6 +23,7 @@
 #include <stdexcept>
 #include <string>
 #include <thread>
+#include <map>
 #include <mutex>
 #include <atomic>
 #include <vector>
@@ -92,12 +93,15 @@ void par_rows(int64_t n, F&& f, int64_t min_rows = 65536) {
 // SparseMatrix invariants (sparse_matrix.cpp:12-32). Rows are checked in
 // parallel; the reported error is the one of the lowest offending row, as a
 // sequential scan would report.
-void validate_csr(const sk_csr* a, const char* what) {
+void validate_csr_header(const sk_csr* a, const char* what) {
   if (!a || !a->row_ptr || (a->nnz > 0 && (!a->col_idx || !a->values)))
     throw SkError(SK_ERR_INVALID_MATRIX, std::string(what) + ": null CSR");
   if (a->n_rows < 0 || a->n_cols < 0) throw SkError(SK_ERR_INVALID_MATRIX, "SparseMatrix: negative dimension");
   if (a->row_ptr[0] != 0 || a->row_ptr[a->n_rows] != a->nnz)
     throw SkError(SK_ERR_INVALID_MATRIX, "SparseMatrix: row_ptr endpoints inconsistent with nnz");
+}
+void validate_csr(const sk_csr* a, const char* what) {
+  validate_csr_header(a, what);
   std::mutex mu;
   int64_t bad_row = INT64_MAX;
   int bad_kind = 0;
@@ -234,8 +238,12 @@ struct StencilInfo {
   int64_t g = 0;
   double c[7] = {0, 0, 0, 0, 0, 0, 0};
 };
-bool detect_stencil(const int64_t* rp, const int64_t* ci, const double* val, int64_t n, StencilInfo& out) {
+// phase 0: full detection; 1: learn the values on the leading rows only (a
+// candidate, out); 2: check the remaining rows against the candidate in out.
+bool detect_stencil(const int64_t* rp, const int64_t* ci, const double* val, int64_t n, StencilInfo& out,
+                    int64_t nnz = INT64_MAX, int phase = 0) {
   for (int dim = 2; dim <= 3; ++dim) {
+    if (phase == 2 && dim != out.dim) continue;
     int64_t g = dim == 2 ? (int64_t)std::llround(std::sqrt((double)n)) : (int64_t)std::llround(std::cbrt((double)n));
     if (g < 2 || (dim == 2 ? g * g : g * g * g) != n) continue;
     const int64_t g2 = g * g;
@@ -261,9 +269,10 @@ bool detect_stencil(const int64_t* rp, const int64_t* ci, const double* val, int
         std::memcpy(present, p, sizeof p);
       }
       int64_t k = rp[i];
+      if (k < 0) return false;
       for (int sl = 0; sl < nslot; ++sl) {
         if (!present[sl]) continue;
-        if (k >= rp[i + 1] || ci[k] != i + off[sl]) return false;
+        if (k >= rp[i + 1] || k >= nnz || ci[k] != i + off[sl]) return false;
         if (learn && !have[sl]) {
           have[sl] = true;
           cval[sl] = val[k];
@@ -278,10 +287,17 @@ bool detect_stencil(const int64_t* rp, const int64_t* ci, const double* val, int
     // values there sequentially, then check all remaining rows in parallel
     const int64_t learn_rows = std::min<int64_t>(n, (dim == 2 ? g : g2) + g + 1);
     bool ok = true;
-    for (int64_t i = 0; i < learn_rows && ok; ++i) ok = row_ok(i, i % g, (i / g) % g, i / g2, true);
-    for (int sl = 0; sl < nslot && ok; ++sl)
-      if (!have[sl] || !std::isfinite(cval[sl])) ok = false;  // absent-neighbour zeros need finite values
-    if (ok) {
+    if (phase == 2) {
+      for (int sl = 0; sl < nslot; ++sl) {
+        have[sl] = true;
+        cval[sl] = out.c[sl];
+      }
+    } else {
+      for (int64_t i = 0; i < learn_rows && ok; ++i) ok = row_ok(i, i % g, (i / g) % g, i / g2, true);
+      for (int sl = 0; sl < nslot && ok; ++sl)
+        if (!have[sl] || !std::isfinite(cval[sl])) ok = false;  // absent-neighbour zeros need finite values
+    }
+    if (ok && phase != 1) {
       std::atomic<bool> all{true};
       par_rows(n - learn_rows, [&](int64_t lo, int64_t hi) {
         const int64_t i0 = lo + learn_rows;
@@ -312,6 +328,49 @@ bool detect_stencil(const int64_t* rp, const int64_t* ci, const double* val, int
   return false;
 }
 
+// SparseMatrix validation (sparse_matrix.cpp:12-32) fused with stencil detection:
+// a CSR whose every row is the grid stencil's (columns i + offset, ascending, in
+// range, row_ptr stepping exactly over them) satisfies every row invariant, so
+// the separate row scan only runs when the operator is not a detected stencil
+// (and reports the same errors, in the same order, as validate_csr).
+//
+// Speculative form (one-shot entry points): only the leading rows that fix the
+// candidate stencil are checked before the solve; the remaining rows are checked
+// on a helper thread while the device solves (SpecCtx). If that check fails, the
+// one-shot call discards its result and reruns the fully checked path, so
+// results and errors are those of the checked path.
+struct SpecCtx {
+  std::vector<std::thread> th;
+  std::atomic<bool> ok{true};
+  void verify(const sk_csr* a, const StencilInfo& cand) {
+    th.emplace_back([this, a, cand] {
+      StencilInfo c = cand;
+      if (!detect_stencil(a->row_ptr, a->col_idx, a->values, a->n_rows, c, a->nnz, 2)) ok = false;
+    });
+  }
+  bool join() {
+    for (auto& t : th)
+      if (t.joinable()) t.join();
+    return ok.load();
+  }
+  ~SpecCtx() { join(); }
+};
+void validate_detect(const sk_csr* a, const char* what, bool use_st, StencilInfo& st, SpecCtx* spec = nullptr) {
+  validate_csr_header(a, what);
+  if (use_st && a->n_rows == a->n_cols) {
+    if (spec) {
+      if (detect_stencil(a->row_ptr, a->col_idx, a->values, a->n_rows, st, a->nnz, 1)) {
+        spec->verify(a, st);
+        return;
+      }
+    } else if (detect_stencil(a->row_ptr, a->col_idx, a->values, a->n_rows, st, a->nnz)) {
+      return;
+    }
+  }
+  st = StencilInfo();
+  validate_csr(a, what);
+}
+
 // a detected grid stencil is bitwise symmetric iff its offsets' values mirror
 // (c(-o) == c(o)): then the CSR equals its transpose entry for entry
 bool stencil_symmetric(const StencilInfo& si) {
@@ -321,37 +380,137 @@ bool stencil_symmetric(const StencilInfo& si) {
   return si.dim != 0;
 }
 
-// Host -> device copy of caller (pageable) memory through two pinned staging
-// buffers: chunk i is copied into buffer i % 2 by all host threads while chunk
-// i - 1 is in flight on the stream (the staging buffers live for the process).
-void h2d_staged(void* dst, const void* src, size_t bytes, cudaStream_t st) {
-  constexpr size_t kChunk = size_t(32) << 20;
-  static std::mutex mu;
-  static char* stage[2] = {nullptr, nullptr};
-  static cudaEvent_t done[2];
-  std::lock_guard<std::mutex> g(mu);
-  if (!stage[0]) {
-    for (int b = 0; b < 2; ++b) {
-      if (cudaHostAlloc(&stage[b], kChunk, cudaHostAllocDefault) != cudaSuccess) {
-        stage[0] = stage[1] = nullptr;
-        CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, st));
-        return;
-      }
-      CK(cudaEventCreateWithFlags(&done[b], cudaEventDisableTiming));
-      CK(cudaEventRecord(done[b], st));
+// keep freed device memory mapped in the default pool across solves (no
+// re-mapping of ~100 GB of basis per solve)
+void keep_pool(int dev) {
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    uint64_t thr = UINT64_MAX;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+}
+
+// Small pinned host buffers (block-pointer tables, status rings) are recycled
+// across solves: cudaHostAlloc / cudaFreeHost cost milliseconds per call and the
+// latter synchronises the device, which the e2e path would pay on every solve.
+struct PinnedPool {
+  std::mutex mu;
+  std::multimap<size_t, void*> free_;
+  std::map<void*, size_t> size_;
+};
+PinnedPool& pinned_pool() {
+  static PinnedPool* p = new PinnedPool();  // never destroyed (driver teardown order)
+  return *p;
+}
+template <class T>
+cudaError_t pinned_alloc(T** out, size_t bytes) {
+  PinnedPool& pp = pinned_pool();
+  {
+    std::lock_guard<std::mutex> g(pp.mu);
+    auto it = pp.free_.lower_bound(bytes);
+    if (it != pp.free_.end() && it->first <= 2 * bytes + 4096) {
+      *out = static_cast<T*>(it->second);
+      pp.free_.erase(it);
+      return cudaSuccess;
     }
   }
-  for (size_t off = 0, i = 0; off < bytes; off += kChunk, ++i) {
-    const size_t n = std::min(kChunk, bytes - off);
-    char* buf = stage[i & 1];
-    CK(cudaEventSynchronize(done[i & 1]));
-    par_rows((int64_t)(n / 4096) + 1, [&](int64_t lo, int64_t hi) {
-      const size_t a = std::min(n, (size_t)lo * 4096), b = std::min(n, (size_t)hi * 4096);
-      if (b > a) std::memcpy(buf + a, (const char*)src + off + a, b - a);
-    }, 256);
-    CK(cudaMemcpyAsync((char*)dst + off, buf, n, cudaMemcpyHostToDevice, st));
-    CK(cudaEventRecord(done[i & 1], st));
+  void* p = nullptr;
+  const cudaError_t e = cudaHostAlloc(&p, bytes, cudaHostAllocDefault);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> g(pp.mu);
+  pp.size_[p] = bytes;
+  *out = static_cast<T*>(p);
+  return cudaSuccess;
+}
+void pinned_free(void* p) {
+  if (!p) return;
+  PinnedPool& pp = pinned_pool();
+  std::lock_guard<std::mutex> g(pp.mu);
+  auto it = pp.size_.find(p);
+  if (it == pp.size_.end()) return;
+  pp.free_.emplace(it->second, p);
+}
+
+// Host -> device copy of caller (pageable) memory: kLanes independent pipelines,
+// each a host thread owning a contiguous slice of the source, two pinned staging
+// buffers and its own stream (memcpy of chunk i into one buffer while chunk i-1's
+// DMA runs from the other). Staging buffers and streams live for the process; the
+// caller's stream waits for every lane's last copy.
+void h2d_staged(void* dst, const void* src, size_t bytes, cudaStream_t st) {
+  constexpr int kMaxLanes = 32;
+  static const int kLanes = [] {
+    const char* e = getenv("SK_H2D_LANES");
+    return std::max(1, std::min(32, e ? std::atoi(e) : 8));
+  }();
+  static const size_t kChunk = [] {
+    const char* e = getenv("SK_H2D_CHUNK_MB");
+    return size_t(std::max(1, e ? std::atoi(e) : 8)) << 20;
+  }();
+  struct Lane {
+    char* buf[2] = {nullptr, nullptr};
+    cudaEvent_t done[2] = {nullptr, nullptr};
+    cudaStream_t s = nullptr;
+    cudaEvent_t fin = nullptr;
+  };
+  static std::mutex mu;
+  static Lane lanes[kMaxLanes];
+  static int dev_init = -1;
+  std::lock_guard<std::mutex> g(mu);
+  int dev = 0;
+  CK(cudaGetDevice(&dev));
+  if (dev_init != dev) {
+    if (dev_init != -1) {  // another device: plain copy (staging is per process, one device)
+      CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, st));
+      return;
+    }
+    for (int li = 0; li < kLanes; ++li) {
+      Lane& L = lanes[li];
+      for (int b = 0; b < 2; ++b) {
+        if (cudaHostAlloc(&L.buf[b], kChunk, cudaHostAllocDefault) != cudaSuccess) {
+          CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, st));
+          return;
+        }
+        CK(cudaEventCreateWithFlags(&L.done[b], cudaEventDisableTiming));
+      }
+      CK(cudaStreamCreateWithFlags(&L.s, cudaStreamNonBlocking));
+      CK(cudaEventCreateWithFlags(&L.fin, cudaEventDisableTiming));
+      for (int b = 0; b < 2; ++b) CK(cudaEventRecord(L.done[b], L.s));
+    }
+    dev_init = dev;
   }
+  const int T = (int)std::max<size_t>(1, std::min<size_t>((size_t)kLanes, (bytes + kChunk - 1) / kChunk));
+  // the copies must not overtake earlier work the caller queued on st
+  cudaEvent_t start;
+  CK(cudaEventCreateWithFlags(&start, cudaEventDisableTiming));
+  CK(cudaEventRecord(start, st));
+  std::vector<std::thread> th;
+  std::string err;
+  std::mutex emu;
+  for (int t = 0; t < T; ++t)
+    th.emplace_back([&, t] {
+      try {
+        CK(cudaSetDevice(dev));
+        Lane& L = lanes[t];
+        CK(cudaStreamWaitEvent(L.s, start, 0));
+        const size_t lo = bytes * t / T, hi = bytes * (t + 1) / T;
+        for (size_t off = lo, i = 0; off < hi; off += kChunk, ++i) {
+          const size_t n = std::min(kChunk, hi - off);
+          char* buf = L.buf[i & 1];
+          CK(cudaEventSynchronize(L.done[i & 1]));
+          std::memcpy(buf, (const char*)src + off, n);
+          CK(cudaMemcpyAsync((char*)dst + off, buf, n, cudaMemcpyHostToDevice, L.s));
+          CK(cudaEventRecord(L.done[i & 1], L.s));
+        }
+        CK(cudaEventRecord(L.fin, L.s));
+      } catch (const std::exception& e) {
+        std::lock_guard<std::mutex> ge(emu);
+        err = e.what();
+      }
+    });
+  for (auto& x : th) x.join();
+  cudaEventDestroy(start);
+  if (!err.empty()) throw SkError(SK_ERR_CUDA, err);
+  for (int t = 0; t < T; ++t) CK(cudaStreamWaitEvent(st, lanes[t].fin, 0));
 }
 
 struct DevCsr {
@@ -683,7 +842,7 @@ struct Solver {
       b.part = dalloc<double>(std::max<int64_t>((cap_blocks + 3) * ncta * s * s, 2 * nseg * s * s + 64));
       b.counter = dalloc<unsigned int>(cap_blocks + 8);
       b.table = dalloc<double*>(cap_blocks);
-      CK(cudaHostAlloc(&b.table_host, sizeof(double*) * cap_blocks, cudaHostAllocDefault));
+      CK(pinned_alloc(&b.table_host, sizeof(double*) * cap_blocks));
       sk::SideConst& sc = c.side[sd];
       sc.n = b.n;
       sc.rp = op.rp;
@@ -1062,7 +1221,7 @@ struct Solver {
     // pinned status ring for asynchronous polling
     const int RING = 64;
     int32_t* hstat = nullptr;
-    CK(cudaHostAlloc(&hstat, sizeof(int32_t) * RING, cudaHostAllocDefault));
+    CK(pinned_alloc(&hstat, sizeof(int32_t) * RING));
     std::vector<cudaEvent_t> rev(RING);
     for (auto& e : rev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     int64_t enq = 0, checked = 0;
@@ -1211,7 +1370,7 @@ struct Solver {
     cudaEventDestroy(t0);
     cudaEventDestroy(t1);
     for (auto& e : rev) cudaEventDestroy(e);
-    cudaFreeHost(hstat);
+    pinned_free(hstat);
     for (auto e : pool) cudaEventDestroy(e);
     pool.clear();
     tr.mark("  device loop");
@@ -1298,7 +1457,7 @@ struct Solver {
     const int64_t batch = pe ? std::max(1, atoi(pe)) : 8;
     const int RING = 64;
     int32_t* hstat = nullptr;
-    CK(cudaHostAlloc(&hstat, sizeof(int32_t) * RING, cudaHostAllocDefault));
+    CK(pinned_alloc(&hstat, sizeof(int32_t) * RING));
     std::vector<cudaEvent_t> rev(RING);
     for (auto& e : rev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     auto cores = [&](int64_t k) {
@@ -1356,7 +1515,7 @@ struct Solver {
     cudaEventDestroy(t0);
     cudaEventDestroy(t1);
     for (auto& e : rev) cudaEventDestroy(e);
-    cudaFreeHost(hstat);
+    pinned_free(hstat);
     for (auto e : pool) cudaEventDestroy(e);
     pool.clear();
     return make_solution(ms, {}, {});
@@ -1396,7 +1555,7 @@ struct Solver {
     dfree(gnodes);
     cudaStreamSynchronize(st);
     for (int sd = 0; sd < nsides; ++sd)
-      if (side[sd].table_host) cudaFreeHost(side[sd].table_host);
+      if (side[sd].table_host) pinned_free(side[sd].table_host);
     dfree(R);
     dfree(P0);
     dfree(P1);
@@ -1475,7 +1634,8 @@ size_t upload_local_csr(DevCsr& d, const int64_t* rp, const int64_t* ci, const d
 }
 
 sk_problem* create_problem(int32_t method, const sk_csr* a, const sk_csr* b, const double* c1,
-                           const double* c2, int64_t s, const sk_gpu_options* gpu, sk::Comm* comm = nullptr) {
+                           const double* c2, int64_t s, const sk_gpu_options* gpu, sk::Comm* comm = nullptr,
+                           SpecCtx* spec = nullptr) {
   HostTrace tr;
   const bool lyap = method == SK_METHOD_CG_LYAPUNOV;
   // C1/C2 go to the device on a helper thread while the host checks run (the
@@ -1488,8 +1648,8 @@ sk_problem* create_problem(int32_t method, const sk_csr* a, const sk_csr* b, con
     std::string err;
     ~EarlyH2D() {
       if (th.joinable()) th.join();
-      if (d1) cudaFree(d1);
-      if (d2) cudaFree(d2);
+      if (d1) cudaFreeAsync(d1, st);
+      if (d2) cudaFreeAsync(d2, st);
       if (st) cudaStreamDestroy(st);
     }
   } early;
@@ -1498,8 +1658,10 @@ sk_problem* create_problem(int32_t method, const sk_csr* a, const sk_csr* b, con
   if (!comm && a && c1 && (lyap || (b && c2)) && s >= 1 && s <= sk::kMaxS && a->n_rows > 0 &&
       cudaGetDeviceCount(&ndev) == cudaSuccess && dev0 >= 0 && dev0 < ndev && cudaSetDevice(dev0) == cudaSuccess) {
     const size_t b1 = sizeof(double) * a->n_rows * s, b2 = lyap ? 0 : sizeof(double) * b->n_rows * s;
+    keep_pool(dev0);  // stream-ordered allocations stay mapped across calls
     if (cudaStreamCreateWithFlags(&early.st, cudaStreamNonBlocking) == cudaSuccess &&
-        cudaMalloc(&early.d1, b1) == cudaSuccess && (lyap || cudaMalloc(&early.d2, b2) == cudaSuccess)) {
+        cudaMallocAsync(&early.d1, b1, early.st) == cudaSuccess &&
+        (lyap || cudaMallocAsync(&early.d2, b2, early.st) == cudaSuccess)) {
       early.th = std::thread([&early, c1, c2, b1, b2, dev0] {
         try {
           CK(cudaSetDevice(dev0));
@@ -1512,8 +1674,11 @@ sk_problem* create_problem(int32_t method, const sk_csr* a, const sk_csr* b, con
       });
     }
   }
-  validate_csr(a, "A");
-  tr.mark("validate A");
+  tr.mark("C1/C2 H2D started");
+  const bool use_st = !getenv("SK_NO_STENCIL");
+  StencilInfo st_a, st_b;
+  validate_detect(a, "A", use_st, st_a, spec);
+  tr.mark("validate + stencil A");
   // B^T: the W basis applies it (block_krylov.cpp:54-56). It is formed on the
   // host only when needed: a bitwise-symmetric B is its own transpose, and the
   // transpose of a grid stencil is the stencil with mirrored coefficients.
@@ -1524,25 +1689,18 @@ sk_problem* create_problem(int32_t method, const sk_csr* a, const sk_csr* b, con
   bool ab_same = false;
   // grid stencils are detected once, up front (a linear pass): a mirror-symmetric
   // stencil is bitwise symmetric without the per-entry search
-  const bool use_st = !getenv("SK_NO_STENCIL");
-  StencilInfo st_a, st_b;
-  if (use_st) detect_stencil(a->row_ptr, a->col_idx, a->values, a->n_rows, st_a);
   auto sym_a = [&] { return stencil_symmetric(st_a) || bitwise_symmetric(a); };
-  tr.mark("stencil detection A");
   if (lyap) {
     if (a->n_rows != a->n_cols) throw SkError(SK_ERR_DIMENSION, "factorized_cg_lyapunov: A must be square");
     if (!sym_a() && !is_symmetric(a, 1e-12))
       throw SkError(SK_ERR_INVALID_MATRIX, "factorized_cg_lyapunov: A is not symmetric");
   } else {
     ab_same = same_csr(a, b);
-    if (!ab_same) validate_csr(b, "B");
+    if (!ab_same) validate_detect(b, "B", use_st, st_b, spec);
     if (a->n_rows != a->n_cols || b->n_rows != b->n_cols)
       throw SkError(SK_ERR_DIMENSION, "solver: A and B must be square");
     if (s < 1) throw SkError(SK_ERR_DIMENSION, "solver: C1 and C2 must have the same positive column count");
-    if (ab_same)
-      st_b = st_a;
-    else if (use_st)
-      detect_stencil(b->row_ptr, b->col_idx, b->values, b->n_rows, st_b);
+    if (ab_same) st_b = st_a;
     if (stencil_symmetric(st_b) || bitwise_symmetric(b)) {
       bt_is_b = true;
     } else if (method == SK_METHOD_BICGSTAB && !comm && st_b.dim) {
@@ -1581,14 +1739,7 @@ sk_problem* create_problem(int32_t method, const sk_csr* a, const sk_csr* b, con
   p->profile = gpu ? gpu->profile : 0;
   p->capacity_bytes = gpu ? gpu->capacity_bytes : 0;
   CK(cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking));
-  {
-    // keep freed basis memory mapped in the pool across solves (no re-mapping per solve)
-    cudaMemPool_t pool;
-    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-      uint64_t thr = UINT64_MAX;
-      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
-    }
-  }
+  keep_pool(dev);
   auto t0 = std::chrono::steady_clock::now();
   if (comm) {
     // row partition: this rank's rows of A and B^T; stencil / halo from the whole operator
@@ -1635,15 +1786,15 @@ sk_problem* create_problem(int32_t method, const sk_csr* a, const sk_csr* b, con
   tr.mark("operators (detect/upload)");
   if (early.th.joinable()) early.th.join();
   if (!early.err.empty()) throw SkError(SK_ERR_CUDA, early.err);
-  if (early.d1) {  // uploaded while the checks ran
+  if (early.d1) {  // uploaded while the checks ran (early.st was synchronised)
     p->c1 = early.d1;
     p->c2 = early.d2;
     early.d1 = early.d2 = nullptr;
   } else {
-    CK(cudaMalloc(&p->c1, sizeof(double) * p->n * s));
+    CK(cudaMallocAsync(&p->c1, sizeof(double) * p->n * s, p->stream));
     h2d_staged(p->c1, c1, sizeof(double) * p->n * s, p->stream);
     if (!lyap) {
-      CK(cudaMalloc(&p->c2, sizeof(double) * p->m * s));
+      CK(cudaMallocAsync(&p->c2, sizeof(double) * p->m * s, p->stream));
       h2d_staged(p->c2, c2, sizeof(double) * p->m * s, p->stream);
     }
   }
@@ -1659,8 +1810,8 @@ void destroy_problem(sk_problem* p) {
   cudaSetDevice(p->device);
   free_csr(p->op[0]);
   if (!p->op_shared) free_csr(p->op[1]);
-  cudaFree(p->c1);
-  cudaFree(p->c2);
+  if (p->c1) cudaFreeAsync(p->c1, p->stream);
+  if (p->c2) cudaFreeAsync(p->c2, p->stream);
   // the stream is shared with solutions; leave it to the process
   delete p;
 }
@@ -1679,7 +1830,25 @@ sk_status one_shot(int32_t method, const sk_csr* a, const sk_csr* b, const doubl
                    sk_solution** out) {
   if (out) *out = nullptr;
   sk_problem* p = nullptr;
-  sk_status rc = run_guarded([&] { p = create_problem(method, a, b, c1, c2, s, gpu); });
+  const bool use_spec = !getenv("SK_NO_SPEC");
+  sk_status rc;
+  {
+    SpecCtx spec;
+    rc = run_guarded([&] { p = create_problem(method, a, b, c1, c2, s, gpu, nullptr, use_spec ? &spec : nullptr); });
+    if (rc == SK_OK) rc = sk_problem_solve(p, cfg, out);
+    if (spec.join()) {
+      destroy_problem(p);
+      return rc;
+    }
+  }
+  // the speculated stencil did not hold on every row: discard and run the checked path
+  if (out && *out) {
+    sk_solution_free(*out);
+    *out = nullptr;
+  }
+  destroy_problem(p);
+  p = nullptr;
+  rc = run_guarded([&] { p = create_problem(method, a, b, c1, c2, s, gpu); });
   if (rc != SK_OK) return rc;
   rc = sk_problem_solve(p, cfg, out);
   destroy_problem(p);

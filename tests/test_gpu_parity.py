@@ -227,3 +227,43 @@ def test_bicgstab_rank_bookkeeping(sk, po):
     assert sol.status == "max_iter" and len(sol.captured_cores) == 4
     for k, core in enumerate(sol.captured_cores):
         assert core.shape == ((2 * k + 2) * 2, (2 * k + 2) * 2)
+
+
+def _stencil_like(po, grid, kind):
+    """laplacian_2d(grid) whose LAST row breaks the stencil (the leading rows that
+    fix the candidate are intact): 'value' keeps a valid symmetric CSR, 'unsorted'
+    makes it invalid."""
+    a = po.laplacian_2d(grid)
+    rp, ci, val = a.row_ptr.copy(), a.col_idx.copy(), a.values.copy()
+    n = a.n_rows
+    k0, k1 = rp[n - 1], rp[n]
+    if kind == "value":
+        val[k1 - 1] = 4.5  # diagonal of the last row (still symmetric)
+    else:
+        ci[k0], ci[k0 + 1] = ci[k0 + 1], ci[k0]
+    return n, rp, ci, val
+
+
+def test_speculative_stencil_falls_back_bitwise(sk, po, monkeypatch):
+    """One-shot calls check only the leading rows before the solve and verify the
+    rest while the device runs; a CSR that stops being the stencil on its last row
+    must give exactly the checked path's result (and the oracle's)."""
+    n, rp, ci, val = _stencil_like(po, 24, "value")
+    a = sk.SparseMatrix(n, n, rp, ci, val)
+    c1, c2 = po.random_dense(n, 2, 31), po.random_dense(n, 2, 32)
+    cfg = _cfg(sk, eps_tol=1e-9)
+    sol = sk.factorized_cg(a, a, c1, c2, cfg)
+    monkeypatch.setenv("SK_NO_SPEC", "1")
+    ref = sk.factorized_cg(a, a, c1, c2, cfg)
+    assert bits_equal(sol.history.rel_residuals(), ref.history.rel_residuals())
+    assert bits_equal(sol.core, ref.core) and bits_equal(sol.V, ref.V)
+    oc = po.Csr(n, n, rp, ci, val)
+    oref = po.factorized_cg(oc, oc, c1, c2, po.Config(eps_tol=1e-9), po.REPRODUCIBLE)
+    assert bits_equal(sol.history.rel_residuals(), oref.rel_residual)
+
+
+def test_speculative_stencil_invalid_row_raises(sk, po):
+    n, rp, ci, val = _stencil_like(po, 24, "unsorted")
+    a = sk.SparseMatrix(n, n, rp, ci, val)
+    with pytest.raises(sk.InvalidMatrixError, match="strictly increasing"):
+        sk.factorized_cg(a, a, po.random_dense(n, 1, 1), po.random_dense(n, 1, 2))

@@ -144,3 +144,18 @@ def test_true_residual_shape_checks_before_device(skl):
     with pytest.raises(skl.DimensionError):
         skl.true_residual_factors(a, a, np.ones((4, 1)), np.ones((4, 2)), np.ones((4, 2)), np.ones((2, 2)),
                                   np.ones((4, 2)))
+
+
+def test_speculative_stencil_invalid_row_raises_without_device(skl):
+    """The one-shot entry points check only a stencil's leading rows before the
+    solve; an invalid later row must still raise the reference's error (here the
+    speculative attempt fails without a device and the checked path reports)."""
+    from paper_2605_28274_b200.problems import laplacian_2d
+    a = laplacian_2d(40)
+    n = a.n_rows
+    ci = a.col_idx.copy()
+    k0 = a.row_ptr[n - 1]
+    ci[k0], ci[k0 + 1] = ci[k0 + 1], ci[k0]
+    bad = skl.SparseMatrix(n, n, a.row_ptr, ci, a.values)
+    with pytest.raises(skl.InvalidMatrixError, match="strictly increasing"):
+        skl.factorized_cg(bad, bad, np.ones((n, 1)), np.ones((n, 1)))
