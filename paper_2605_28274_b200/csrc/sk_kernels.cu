@@ -746,9 +746,12 @@ __global__ void __launch_bounds__(256) k_gram(const __grid_constant__ SolveConst
   if (!gram_setup<S>(c, side, mode, x, out, mout, b0, b1)) return;
   const SideConst& sc = c.side[side];
   const int64_t nblk = b1 - b0;
-  const int64_t by = blockIdx.y;
+  // grid x runs over the blocks, y over row ranges: the CTAs that are resident
+  // together share a row range, so x's rows stay in L2 across all blocks (one
+  // HBM read of x per pass instead of one per block)
+  const int64_t by = blockIdx.x;
   if (by >= nblk) return;
-  const int64_t cta = blockIdx.x;
+  const int64_t cta = blockIdx.y;
   if (cta >= sc.ncta) return;
   const int64_t b = b0 + by;
   const double* __restrict__ ub = sc.blocks[b];
@@ -1776,7 +1779,7 @@ __device__ __forceinline__ const double* blk_ptr(const SideConst& sc, int64_t b)
 }
 template <int S>
 __global__ void __launch_bounds__(kArnThreads) k_arn_update(const __grid_constant__ SolveConst c, int mode) {
-  constexpr int UN = 8;
+  constexpr int UN = S <= 2 ? 8 : (S <= 4 ? 4 : 2);   // block rows in flight (registers: 2*UN*S)
   constexpr int CH = (S <= 2 ? 1024 : 4096 / (S * S));  // M chunk (blocks), multiple of UN
   const int side = blockIdx.y;
   if (side >= c.nsides) return;
@@ -2830,7 +2833,7 @@ struct Launch {
   static void gram(const SolveConst& c, int mode, int64_t nblk, cudaStream_t st) {
     int64_t nmax, cmax;
     dims(c, nmax, cmax);
-    k_gram<S><<<dim3((unsigned)cmax, (unsigned)(nblk > 0 ? nblk : 1), c.nsides), 256, 0, st>>>(c, mode);
+    k_gram<S><<<dim3((unsigned)(nblk > 0 ? nblk : 1), (unsigned)cmax, c.nsides), 256, 0, st>>>(c, mode);
   }
   static void update(const SolveConst& c, int mode, cudaStream_t st) {
     int64_t nmax, cmax;
