@@ -56,7 +56,8 @@ typedef enum {
     SK_ERR_CUDA = -10,           /* CUDA runtime failure, or no device       */
     SK_ERR_OUT_OF_MEMORY = -11,
     SK_ERR_CAPACITY = -12,       /* basis budget exceeded before max_iter    */
-    SK_ERR_UNSUPPORTED = -13     /* e.g. block size s > 8 on the device path */
+    SK_ERR_UNSUPPORTED = -13,    /* e.g. block size s > 8 on the device path */
+    SK_ERR_IO = -14              /* IoError                (errors.hpp:48-51) */
 } sk_status;
 
 /* SolveStatus (solver_types.hpp:11) */
@@ -120,6 +121,10 @@ double sk_solution_total_time(const sk_solution* sol);
 sk_status sk_solution_copy_V(const sk_solution* sol, double* out);    /* n  x rv */
 sk_status sk_solution_copy_core(const sk_solution* sol, double* out); /* rv x rw */
 sk_status sk_solution_copy_W(const sk_solution* sol, double* out);    /* m  x rw */
+/* Column ranges [col0, col0 + ncols) of V / W (n x ncols, m x ncols column-major):
+ * only the basis blocks covering the range leave HBM. */
+sk_status sk_solution_copy_V_cols(const sk_solution* sol, int64_t col0, int64_t ncols, double* out);
+sk_status sk_solution_copy_W_cols(const sk_solution* sol, int64_t col0, int64_t ncols, double* out);
 int64_t sk_solution_num_captured(const sk_solution* sol);
 sk_status sk_solution_captured_core(const sk_solution* sol, int64_t i, int64_t* rows,
                                     int64_t* cols, double* out);
@@ -197,6 +202,25 @@ sk_status sk_gen_stencil(int32_t kind, int64_t grid, const double* wind, int64_t
                          int64_t* col_idx, double* values);
 /* random_rhs: rows x s column-major, std::mt19937_64 + Box-Muller (bitwise the reference's). */
 sk_status sk_gen_random_rhs(int64_t rows, int64_t s, uint64_t seed, double* out);
+
+/* On-disk formats. Text is byte-identical to the reference's
+ * writers (17 significant digits, "%.17g"); all return SK_ERR_IO on a failed
+ * open or write, with the path in sk_last_error().
+ *   sk_write_history_csv         -- write_history_csv   (bench.cpp:179-193)
+ *   sk_write_matrix_market_csr   -- write_matrix_market(SparseMatrix) (matrix_market.cpp:148-161)
+ *   sk_write_matrix_market_dense -- write_matrix_market(DenseMatrix)  (matrix_market.cpp:163-175)
+ *   sk_solution_write_factors    -- the V.mtx / core.mtx / W.mtx triple of the CLI
+ *     (main.cpp:182-184) into directory dir (which must exist), streamed from HBM
+ *     block by block and formatted on all host threads; format SK_FORMAT_BINARY
+ *     writes V.skb / core.skb / W.skb instead: the binary sidecar for solutions
+ *     whose text form would not fit a disk (C5: ~170 GB of text), layout =
+ *     8-byte magic "SKFACT01", int64 rows, int64 cols, rows*cols little-endian
+ *     fp64 column-major. */
+enum { SK_FORMAT_MATRIX_MARKET = 0, SK_FORMAT_BINARY = 1 };
+sk_status sk_write_history_csv(const sk_solution* sol, const char* path);
+sk_status sk_write_matrix_market_csr(const sk_csr* a, const char* path);
+sk_status sk_write_matrix_market_dense(const double* a, int64_t rows, int64_t cols, const char* path);
+sk_status sk_solution_write_factors(const sk_solution* sol, const char* dir, int32_t format);
 
 #ifdef __cplusplus
 }

@@ -9,6 +9,7 @@ REF=/root/reference/proj
 [ -d "$REF/src" ] || { echo "reference sources absent; skipping"; exit 0; }
 mkdir -p "$HERE/_ref"
 g++ -std=c++20 -O3 -Wall -Wextra -fPIC -shared -pthread -I"$REF/include" \
-    "$REF/src/sparse_matrix.cpp" "$REF/src/parallel.cpp" "$REF/src/problems.cpp" "$HERE/ref_capi.cpp" \
+    "$REF/src/sparse_matrix.cpp" "$REF/src/parallel.cpp" "$REF/src/problems.cpp" \
+    "$REF/src/matrix_market.cpp" "$HERE/ref_capi.cpp" \
     -o "$HERE/_ref/libsylkrylov_ref.so"
 echo "$HERE/_ref/libsylkrylov_ref.so"

@@ -1,5 +1,5 @@
 // C entry points over the reference's own Eigen-free sources (compiled from
-// /root/reference/proj/src/{sparse_matrix,parallel,problems}.cpp by
+// /root/reference/proj/src/{sparse_matrix,parallel,problems,matrix_market}.cpp by
 // oracle/build_ref.sh into oracle/_ref/). TEST INFRASTRUCTURE: used only to pin
 // the oracle's restatement of SpMM, CSR utilities and generators bitwise.
 #include <cstring>
@@ -7,6 +7,7 @@
 
 #include "sylkrylov/dense_matrix.hpp"
 #include "sylkrylov/errors.hpp"
+#include "sylkrylov/matrix_market.hpp"
 #include "sylkrylov/parallel.hpp"
 #include "sylkrylov/problems.hpp"
 #include "sylkrylov/sparse_matrix.hpp"
@@ -73,4 +74,34 @@ int ref_is_symmetric(int64_t nr, int64_t nc, int64_t nnz, const int64_t* rp, con
     return import_csr(nr, nc, nnz, rp, ci, v).is_symmetric(tol) ? 1 : 0;
 }
 void ref_set_parallel(int enabled, unsigned threads) { set_parallel_kernels(enabled != 0, threads); }
+// Matrix Market writers / reader (matrix_market.cpp): 0 ok, -1 on any exception
+int ref_write_mm_csr(int64_t nr, int64_t nc, int64_t nnz, const int64_t* rp, const int64_t* ci, const double* v,
+                     const char* path) {
+    try {
+        write_matrix_market(import_csr(nr, nc, nnz, rp, ci, v), path);
+        return 0;
+    } catch (...) {
+        return -1;
+    }
+}
+int ref_write_mm_dense(int64_t rows, int64_t cols, const double* x, const char* path) {
+    try {
+        write_matrix_market(import_dense(rows, cols, x), path);
+        return 0;
+    } catch (...) {
+        return -1;
+    }
+}
+// sparse read: call with null buffers for the sizes (n_rows, n_cols, nnz), then with buffers
+int64_t ref_read_mm_csr(const char* path, int64_t* dims, int64_t* rp, int64_t* ci, double* v) {
+    try {
+        SparseMatrix a = read_matrix_market_sparse(path);
+        dims[0] = a.rows();
+        dims[1] = a.cols();
+        dims[2] = a.nnz();
+        return export_csr(a, rp, ci, v);
+    } catch (...) {
+        return -1;
+    }
+}
 }

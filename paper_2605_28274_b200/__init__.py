@@ -56,8 +56,17 @@ class UnsupportedError(SylkrylovError):
     code = -13
 
 
+class IoError(SylkrylovError, OSError):
+    """errors.hpp:48-51 (a failed open or write of an output file)."""
+    code = -14
+
+
+class ParseError(SylkrylovError, ValueError):
+    """errors.hpp:54-57 (malformed Matrix Market input)."""
+
+
 _ERRORS = {e.code: e for e in [DimensionError, InvalidMatrixError, RankDeficientStartError,
-                                CudaError, OutOfMemoryError, CapacityError, UnsupportedError]}
+                                CudaError, OutOfMemoryError, CapacityError, UnsupportedError, IoError]}
 
 
 class _Csr(C.Structure):
@@ -277,6 +286,18 @@ class FactorizedSolution:
             self._core = np.zeros((self.rv, self.rw), order="F")
             _check(lib().sk_solution_copy_core(self._h, _p(self._core)))
         return self._core
+
+    def write_factors(self, out_dir: str, fmt: str = "mtx") -> None:
+        """V / core / W files of the CLI (main.cpp:182-184), streamed from HBM:
+        fmt "mtx" = Matrix Market text (V.mtx, core.mtx, W.mtx), "binary" = the
+        binary sidecar (V.skb, core.skb, W.skb; read back with read_factor)."""
+        os.makedirs(out_dir, exist_ok=True)
+        code = {"mtx": 0, "binary": 1}[fmt]
+        _check(lib().sk_solution_write_factors(self._h, os.fsencode(out_dir), C.c_int32(code)))
+
+    def write_history_csv(self, path: str) -> None:
+        """write_history_csv (bench.cpp:179-193), byte-identical format."""
+        _check(lib().sk_write_history_csv(self._h, os.fsencode(path)))
 
     def free(self):
         if getattr(self, "_h", None):
@@ -545,3 +566,121 @@ def solve_local_group(method: str, a: SparseMatrix, b: Optional[SparseMatrix], c
     for p in probs:
         p.free()
     return sols
+
+
+# ---- on-disk formats (matrix_market.cpp, bench.cpp:179-193, main.cpp:146-239) ----
+def write_matrix_market(m, path: str) -> None:
+    """write_matrix_market (matrix_market.cpp:148-175): a SparseMatrix as
+    "coordinate real general", a 2-D array as "array real general" (column-major),
+    17 significant digits. Formatting runs natively on all host threads."""
+    if isinstance(m, SparseMatrix):
+        cm = m._c()
+        _check(lib().sk_write_matrix_market_csr(C.byref(cm), os.fsencode(path)))
+        return
+    a = np.asfortranarray(np.asarray(m, dtype=np.float64))
+    if a.ndim != 2:
+        raise DimensionError("write_matrix_market: a 2-D array is required")
+    _check(lib().sk_write_matrix_market_dense(_p(a), C.c_int64(a.shape[0]), C.c_int64(a.shape[1]),
+                                              os.fsencode(path)))
+
+
+def read_matrix_market(path: str):
+    """read_matrix_market (matrix_market.cpp:1-138 restated): coordinate real
+    general/symmetric -> SparseMatrix (symmetric storage expanded, duplicates
+    summed, columns sorted as from_triplets, sparse_matrix.cpp:34-69); array real
+    general -> column-major ndarray. Anything else raises ParseError."""
+    with open(path) as f:
+        header = f.readline()
+        tok = header.split()
+        if len(tok) < 5 or tok[0].lower() != "%%matrixmarket" or tok[1].lower() != "matrix":
+            raise ParseError(f"{path}: malformed MatrixMarket header: {header.rstrip()}")
+        fmt, field, sym = tok[2].lower(), tok[3].lower(), tok[4].lower()
+        if fmt not in ("coordinate", "array"):
+            raise ParseError(f"{path}: unsupported format '{tok[2]}'")
+        if field != "real":
+            raise ParseError(f"{path}: unsupported field '{tok[3]}' (real required)")
+        if sym not in ("general", "symmetric"):
+            raise ParseError(f"{path}: unsupported symmetry '{tok[4]}'")
+        if fmt == "array" and sym == "symmetric":
+            raise ParseError(f"{path}: array symmetric storage not supported")
+        lines = [ln for ln in f.read().splitlines() if ln.strip() and not ln.lstrip().startswith("%")]
+    if not lines:
+        raise ParseError(f"{path}: missing size line")
+    size = lines[0].split()
+    try:
+        if fmt == "array":
+            rows, cols = int(size[0]), int(size[1])
+            vals = np.array([float(x) for x in lines[1:]], dtype=np.float64)
+            if vals.size != rows * cols:
+                raise ParseError(f"{path}: expected {rows * cols} values, found {vals.size}")
+            return vals.reshape((rows, cols), order="F")
+        rows, cols, nnz = int(size[0]), int(size[1]), int(size[2])
+        ent = np.array([ln.split()[:3] for ln in lines[1:]], dtype=np.float64).reshape(-1, 3)
+    except (ValueError, IndexError) as e:
+        raise ParseError(f"{path}: {e}") from None
+    if ent.shape[0] != nnz:
+        raise ParseError(f"{path}: expected {nnz} entries, found {ent.shape[0]}")
+    i = ent[:, 0].astype(np.int64) - 1
+    j = ent[:, 1].astype(np.int64) - 1
+    v = ent[:, 2]
+    if ((i < 0) | (i >= rows) | (j < 0) | (j >= cols)).any():
+        raise ParseError(f"{path}: entry index out of range")
+    if sym == "symmetric":
+        off = i != j
+        i, j, v = np.concatenate([i, j[off]]), np.concatenate([j, i[off]]), np.concatenate([v, v[off]])
+    order = np.lexsort((j, i))
+    i, j, v = i[order], j[order], v[order]
+    key = i * cols + j
+    first = np.ones(key.size, dtype=bool)
+    first[1:] = key[1:] != key[:-1]
+    # duplicates summed (from_triplets; the reference's std::sort leaves their order unspecified)
+    vs = np.add.reduceat(v, np.flatnonzero(first)) if v.size else v.copy()
+    ii, jj = i[first], j[first]
+    row_ptr = np.zeros(rows + 1, dtype=np.int64)
+    np.add.at(row_ptr, ii + 1, 1)
+    return SparseMatrix(rows, cols, np.cumsum(row_ptr), jj.astype(np.int64), vs)
+
+
+def read_factor(path: str) -> np.ndarray:
+    """Reads a binary sidecar written by FactorizedSolution.write_factors(fmt="binary")."""
+    with open(path, "rb") as f:
+        if f.read(8) != b"SKFACT01":
+            raise ParseError(f"{path}: not a factor sidecar")
+        rows, cols = np.frombuffer(f.read(16), dtype="<i8")
+        data = np.frombuffer(f.read(), dtype="<f8")
+    if data.size != rows * cols:
+        raise ParseError(f"{path}: truncated ({data.size} of {rows * cols} values)")
+    return data.reshape((int(rows), int(cols)), order="F")
+
+
+def write_solution(out_dir: str, method: str, sol: FactorizedSolution, a: SparseMatrix, b: SparseMatrix,
+                   c1, c2, cfg: Optional["SolverConfig"] = None, inputs: Optional[dict] = None,
+                   seed: Optional[int] = None, fmt: str = "mtx", lyapunov: bool = False) -> dict:
+    """The output directory of `sylkrylov solve` for the factorized methods
+    (main.cpp:146-239): V/core/W, history.csv and meta.json with the same keys
+    (the true residual is computed on the device). Returns the meta dict."""
+    import json
+    import math
+    cfg = cfg or SolverConfig()
+    os.makedirs(out_dir, exist_ok=True)
+    residual = true_residual(a, b, c1, c2, sol)
+    sol.write_factors(out_dir, fmt)
+    sol.write_history_csv(os.path.join(out_dir, "history.csv"))
+    recs = sol.history.records
+    # resolve_max_iter (solver_types.cpp:34-38)
+    max_iter = cfg.max_iter if cfg.max_iter > 0 else min(10 * math.ceil(math.sqrt(float(a.n_rows) * float(b.n_rows))),
+                                                         10000)
+    meta = {"method": method, "eps_tol": cfg.eps_tol, "max_iter": max_iter,
+            "lyapunov": lyapunov, "inputs": inputs or {},
+            "format": "factored", "status": sol.status, "iterations": sol.history.iterations(),
+            "final_true_residual": residual,
+            "ranks": {"rank": min(sol.rv, sol.rw), "v_cols": sol.rv, "w_cols": sol.rw},
+            "timings": {"total_s": sol.history.total_time_s,
+                        "basic_s": sum(r.t_basic_s for r in recs),
+                        "krylov_s": sum(r.t_krylov_s for r in recs),
+                        "trunc_s": sum(r.t_trunc_s for r in recs)}}
+    if seed is not None:
+        meta["seed"] = seed
+    with open(os.path.join(out_dir, "meta.json"), "w") as f:
+        f.write(json.dumps(meta, indent=2, sort_keys=True) + "\n")
+    return meta

@@ -33,6 +33,7 @@ def units():
     u.append(("sk_residual.cu", "sk_residual.o", []))
     u.append(("sk_problems.cpp", "sk_problems.o", []))
     u.append(("sk_comm.cpp", "sk_comm.o", []))
+    u.append(("sk_export.cpp", "sk_export.o", []))
     return [(src, obj.replace(".o", OBJ_SUFFIX + ".o"), defs + EXTRA_DEFS) for src, obj, defs in u]
 
 
@@ -50,7 +51,7 @@ def _compile(unit, verbose):
     src, obj, defs = unit
     if src.endswith(".cpp"):
         cmd = ["g++", "-O3", "-std=c++17", "-fPIC", "-Wall", "-ffp-contract=off", "-pthread",
-               "-I/usr/local/cuda/include", *defs,
+               "-I/usr/local/cuda/include", "-I" + os.path.join(HERE, "..", "include"), *defs,
                "-c", os.path.join(CSRC, src), "-o", os.path.join(CSRC, obj)]
     else:
         cmd = [NVCC, *FLAGS, *defs, "-c", os.path.join(CSRC, src), "-o", os.path.join(CSRC, obj)]

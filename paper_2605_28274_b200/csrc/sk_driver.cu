@@ -2314,6 +2314,38 @@ static sk_status copy_basis(const sk_solution* sol, const std::vector<double*>& 
     cudaFree(stage);
   });
 }
+// columns [col0, col0 + ncols) of a basis: only the blocks covering them are
+// exported (the streaming writers of sk_export.cpp never hold all of V on the host)
+static sk_status copy_basis_cols(const sk_solution* sol, const std::vector<double*>& blocks,
+                                 const double* nfac, int64_t n, int64_t cols, int64_t col0, int64_t ncols,
+                                 double* out) {
+  if (col0 < 0 || ncols < 0 || col0 + ncols > cols) {
+    g_err = "copy_cols: column range out of bounds";
+    return SK_ERR_DIMENSION;
+  }
+  return run_guarded([&] {
+    CK(cudaSetDevice(sol->device));
+    if (ncols == 0) return;
+    double* stage = nullptr;
+    CK(cudaMalloc(&stage, sizeof(double) * n * sol->s));
+    const int64_t s = sol->s;
+    for (int64_t b = col0 / s; b * s < col0 + ncols; ++b) {
+      sk::launch_export_block((int)s, blocks[b], nfac, b, stage, n, sol->stream);
+      const int64_t c0 = std::max(col0, b * s), c1 = std::min(col0 + ncols, (b + 1) * s);
+      CK(cudaMemcpyAsync(out + (c0 - col0) * n, stage + (c0 - b * s) * n, sizeof(double) * n * (c1 - c0),
+                         cudaMemcpyDeviceToHost, sol->stream));
+    }
+    CK(cudaStreamSynchronize(sol->stream));
+    cudaFree(stage);
+  });
+}
+sk_status sk_solution_copy_V_cols(const sk_solution* sol, int64_t col0, int64_t ncols, double* out) {
+  return copy_basis_cols(sol, sol->vblocks, sol->vnfac, sol->n, sol->rv, col0, ncols, out);
+}
+sk_status sk_solution_copy_W_cols(const sk_solution* sol, int64_t col0, int64_t ncols, double* out) {
+  return copy_basis_cols(sol, sol->wblocks, sol->wnfac, sol->m, sol->rw, col0, ncols, out);
+}
+void sk_internal_set_error(const char* msg) { g_err = msg; }
 sk_status sk_solution_copy_V(const sk_solution* sol, double* out) {
   return copy_basis(sol, sol->vblocks, sol->vnfac, sol->n, sol->rv, out);
 }

@@ -1299,7 +1299,13 @@ __global__ void __launch_bounds__(kFusedThreads, kWaveBlocks)
 // k_lanczos_p2 / k_lanczos_p1.
 // =====================================================================
 #ifndef SK_CS_NC
-#define SK_CS_NC 1
+#define SK_CS_NC 2
+#endif
+#ifndef SK_CS_CARRY
+#define SK_CS_CARRY 1
+#endif
+#ifndef SK_CS_TMA
+#define SK_CS_TMA 1
 #endif
 constexpr int kCsNC = SK_CS_NC;            // grid columns per column thread
 constexpr int kCsColWarps = 16 / kCsNC;    // 512 columns
@@ -1327,6 +1333,30 @@ __device__ __forceinline__ void cs_copy(double* dst, const double* src, bool ok)
   }
 }
 __device__ __forceinline__ void cs_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+// bulk (TMA) line copies completing on an mbarrier
+__device__ __forceinline__ void mb_init(uint64_t* mb) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"((unsigned)__cvta_generic_to_shared(mb)) : "memory");
+}
+__device__ __forceinline__ void mb_expect_arrive(uint64_t* mb, unsigned tx) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"((unsigned)__cvta_generic_to_shared(mb)),
+               "r"(tx)
+               : "memory");
+}
+__device__ __forceinline__ void mb_wait(uint64_t* mb, unsigned parity) {
+  const unsigned a = (unsigned)__cvta_generic_to_shared(mb);
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      "W: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra W;\n}" ::"r"(a),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* mb) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   (unsigned)__cvta_generic_to_shared(dst)),
+               "l"(src), "r"(bytes), "r"((unsigned)__cvta_generic_to_shared(mb))
+               : "memory");
+}
 __device__ __forceinline__ void cs_wait3() { asm volatile("cp.async.wait_group 3;" ::: "memory"); }
 // 0 + c0 up + c1 left + c2 centre + c3 right + c4 down (CSR order, mul then add)
 template <int S>
@@ -1391,6 +1421,11 @@ __global__ void __launch_bounds__(kCsThreads, 1)
     k_lanczos_cols(const __grid_constant__ SolveConst c, int side0, int nranges) {
   constexpr int NS = S * (S + 1) / 2, NB = S * S, NE = NS + 2 * NB;
   constexpr int AL = kCsA * S, KL = kCsK * S, ZL = kSeg * S;  // ring line strides (doubles)
+#if SK_CS_TMA
+  constexpr int BL = AL, BO = 2;  // U_{k-2} lines span the same columns as U_{k-1} (16-byte aligned rows)
+#else
+  constexpr int BL = KL, BO = 1;
+#endif
   const int side = side0 + blockIdx.y;
   if (side >= c.nsides) return;
   DevState* st = c.st;
@@ -1413,7 +1448,7 @@ __global__ void __launch_bounds__(kCsThreads, 1)
   extern __shared__ __align__(16) double cs_smem[];
   double* Ar = cs_smem;                    // [kCsAR][AL]
   double* Br = Ar + kCsAR * AL;            // [kCsBR][KL]
-  double* Kb = Br + kCsBR * KL;            // [kCsKR][KL]
+  double* Kb = Br + kCsBR * BL;            // [kCsKR][KL]
   double* Zs = Kb + kCsKR * KL;            // [2][ZL]
   __shared__ NF<S> f1s;
   __shared__ double m1[NB], m0[NB];
@@ -1448,6 +1483,7 @@ __global__ void __launch_bounds__(kCsThreads, 1)
   const double* U0 = two ? sc.blocks[k - 2] : U1;
   double* UK = sc.blocks[k];
   const int ys = y0 - 1;
+#if !SK_CS_TMA
   // copies of line ya of U_{k-1} (and line yb of U_{k-2}) for this thread's columns
   auto copy_a = [&](int ya) {
     double* d = Ar + (ya & (kCsAR - 1)) * AL;
@@ -1457,12 +1493,62 @@ __global__ void __launch_bounds__(kCsThreads, 1)
       if (q < nslot) cs_copy<S>(d + (xs[q] - x0 + 2) * S, U1 + ((int64_t)ya * g + (cv[q] ? xs[q] : 0)) * S, lok && cv[q]);
   };
   auto copy_b = [&](int yb) {
-    double* d = Br + (yb & (kCsBR - 1)) * KL;
+    double* d = Br + (yb & (kCsBR - 1)) * BL;
     const bool lok = two && yb >= 0 && yb < g;
 #pragma unroll
     for (int q = 0; q < kCsNC; ++q)
-      if (q < nslot) cs_copy<S>(d + (xs[q] - x0 + 1) * S, U0 + ((int64_t)yb * g + (cv[q] ? xs[q] : 0)) * S, lok && cv[q]);
+      if (q < nslot) cs_copy<S>(d + (xs[q] - x0 + BO) * S, U0 + ((int64_t)yb * g + (cv[q] ? xs[q] : 0)) * S, lok && cv[q]);
   };
+#endif
+#if SK_CS_TMA
+  // line loads by one thread (reducer warp 0, lane 0) as bulk copies: group t
+  // (issued at step ys + t - 4, consumed at step ys + t) completes on mbarrier
+  // mbar[t & 7]. Columns outside the grid stay zero (written once here); lines
+  // outside the grid are zero-filled by the issuing warp.
+  __shared__ __align__(8) uint64_t mbar[8];
+  const bool issuer = warp == kCsColWarps + 1;
+  const int ca = x0 - 2 < 0 ? 0 : x0 - 2, cb = x0 + kSeg + 1 >= g ? g - 1 : x0 + kSeg + 1;
+  const unsigned lbytes = (unsigned)((cb - ca + 1) * S * 8);
+  if (threadIdx.x < 8) mb_init(&mbar[threadIdx.x]);
+  for (int i = threadIdx.x; i < kCsAR + kCsBR; i += blockDim.x) {
+    double* d = Ar + i * AL;  // Br follows Ar with the same stride
+#pragma unroll
+    for (int t = 0; t < 2 * S; ++t) {
+      if (x0 == 0) d[t] = 0.0;
+      if (x0 + kSeg >= g) d[(kCsA - 2) * S + t] = 0.0;
+    }
+  }
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  __syncthreads();
+  // the issuing warp: one group = U_{k-1} lines [la0, la1] and U_{k-2} line lb (lb < 0: none)
+  auto issue = [&](int t, int la0, int la1, int lb) {
+    unsigned tx = 0;
+    for (int ya = la0; ya <= la1; ++ya) tx += (ya >= 0 && ya < g) ? lbytes : 0u;
+    const bool bok = two && lb >= 0 && lb < g;
+    tx += bok ? lbytes : 0u;
+    for (int ya = la0; ya <= la1; ++ya)
+      if (ya < 0 || ya >= g) {
+        double* d = Ar + (ya & (kCsAR - 1)) * AL;
+        for (int i = lane; i < AL; i += 32) d[i] = 0.0;
+      }
+    __syncwarp();
+    if (lane == 0) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      uint64_t* mb = &mbar[t & 7];
+      mb_expect_arrive(mb, tx);
+      for (int ya = la0; ya <= la1; ++ya)
+        if (ya >= 0 && ya < g)
+          bulk_g2s(Ar + (ya & (kCsAR - 1)) * AL + (ca - x0 + 2) * S, U1 + ((int64_t)ya * g + ca) * S, lbytes, mb);
+      if (bok)
+        bulk_g2s(Br + (lb & (kCsBR - 1)) * BL + (ca - x0 + 2) * S, U0 + ((int64_t)lb * g + ca) * S, lbytes, mb);
+    }
+  };
+  // prologue: U_{k-1} lines ys-3 .. ys+4, U_{k-2} lines ys .. ys+3 (groups 0 .. 3)
+  if (issuer) {
+    issue(0, ys - 3, ys + 1, ys);
+    for (int t = 1; t < 4; ++t) issue(t, ys + t + 1, ys + t + 1, ys + t);
+  }
+#else
   __syncthreads();
   // prologue: U_{k-1} lines ys-3 .. ys+4, U_{k-2} lines ys .. ys+3 (groups G(ys-4) .. G(ys-1))
   if (nslot) {
@@ -1473,22 +1559,42 @@ __global__ void __launch_bounds__(kCsThreads, 1)
     if (compute) copy_b(v + 4);
     cs_commit();
   }
+#endif
   double* gseg = sc.spart;                              // [g * nstrip][NE] segment partials
   double* lnode = sc.spart + (int64_t)g * nstrip * NE;  // [g][NE] line nodes
 
+#if SK_CS_CARRY
+  // a thread's own column is carried down the lines in registers: U_{k-1} lines
+  // y-1, y (up, centre of the next stencil) and U_k lines y-2, y-1 (its own
+  // earlier outputs); only the neighbours and the new lines come from shared memory
+  double cup[kCsNC][S], cce[kCsNC][S], kup[kCsNC][S], kce[kCsNC][S];
+#pragma unroll
+  for (int q = 0; q < kCsNC; ++q)
+#pragma unroll
+    for (int t = 0; t < S; ++t) cup[q][t] = cce[q][t] = kup[q][t] = kce[q][t] = 0.0;
+#endif
   // steps for lines y0-1 .. y1 (U_k with one halo line each side) + one drain step
   for (int y = ys; y <= y1 + 1; ++y) {
+#if SK_CS_TMA
+    if (issuer && lane == 0) mb_wait(&mbar[(y - ys) & 7], (unsigned)((y - ys) >> 3) & 1u);
+    __syncthreads();
+    // group G(y): U_{k-1} line y + 5, U_{k-2} line y + 4 (consumed at step y + 4;
+    // the slots' last readers finished before this step's barrier)
+    if (issuer && y + 4 <= y1 + 1) issue(y - ys + 4, y + 5, y + 5, y + 4);
+#else
     asm volatile("cp.async.wait_group 3;" ::: "memory");
     __syncthreads();
+#endif
     if (warp <= kCsColWarps) {
       if (compute && y <= y1) {
         const double* Am = Ar + ((y - 1) & (kCsAR - 1)) * AL;
         const double* A0 = Ar + (y & (kCsAR - 1)) * AL;
         const double* Ap = Ar + ((y + 1) & (kCsAR - 1)) * AL;
-        const double* B0 = Br + (y & (kCsBR - 1)) * KL;
+        const double* B0 = Br + (y & (kCsBR - 1)) * BL;
         double* K0 = Kb + (y & (kCsKR - 1)) * KL;
         const double* K1 = Kb + ((y - 1) & (kCsKR - 1)) * KL;
         const double* K2 = Kb + ((y - 2) & (kCsKR - 1)) * KL;
+        (void)K2;
         double* Z1 = Zs + ((y - 1) & 1) * ZL;
         const bool zl = inner && y - 1 >= y0 && y - 1 < y1;
         const bool wr = inner && y >= y0 && y < y1;
@@ -1501,9 +1607,17 @@ __global__ void __launch_bounds__(kCsThreads, 1)
             double v[S], z2[S];
             {
               double up[S], le[S], ce[S], ri[S];
+#if SK_CS_CARRY
+#pragma unroll
+              for (int t = 0; t < S; ++t) {
+                up[t] = kup[q][t];
+                ce[t] = kce[q][t];
+              }
+#else
               sw_get<S>(K2 + ki, up);
-              sw_get<S>(K1 + ki - S, le);
               sw_get<S>(K1 + ki, ce);
+#endif
+              sw_get<S>(K1 + ki - S, le);
               sw_get<S>(K1 + ki + S, ri);
               // z' = op U_k on line y - 1: the first four terms, the down term below
 #pragma unroll
@@ -1516,13 +1630,32 @@ __global__ void __launch_bounds__(kCsThreads, 1)
             }
             {
               double up[S], le[S], ce[S], ri[S], dn[S], z[S], bb[S];
+#if SK_CS_CARRY
+              if (y == ys) {
+                sw_get<S>(Am + ai, cup[q]);
+                sw_get<S>(A0 + ai, cce[q]);
+              }
+#pragma unroll
+              for (int t = 0; t < S; ++t) {
+                up[t] = cup[q][t];
+                ce[t] = cce[q][t];
+              }
+#else
               sw_get<S>(Am + ai, up);
-              sw_get<S>(A0 + ai - S, le);
               sw_get<S>(A0 + ai, ce);
+#endif
+              sw_get<S>(A0 + ai - S, le);
               sw_get<S>(A0 + ai + S, ri);
               sw_get<S>(Ap + ai, dn);
-              sw_get<S>(B0 + ki, bb);
+              sw_get<S>(B0 + ai + (BO - 2) * S, bb);
               cs_stencil<S>(sc.scoef, up, le, ce, ri, dn, z);
+#if SK_CS_CARRY
+#pragma unroll
+              for (int t = 0; t < S; ++t) {
+                cup[q][t] = ce[t];
+                cce[q][t] = dn[t];
+              }
+#endif
               norm_row<S>(z, f1s, v);
               if (two) {
 #pragma unroll
@@ -1547,6 +1680,13 @@ __global__ void __launch_bounds__(kCsThreads, 1)
             }
             if (wr) st_row<S>(UK + ((int64_t)y * g + xs[q]) * S, 0, v);
             sw_put<S>(K0 + ki, v);
+#if SK_CS_CARRY
+#pragma unroll
+            for (int t = 0; t < S; ++t) {
+              kup[q][t] = kce[q][t];
+              kce[q][t] = v[t];
+            }
+#endif
             if (zl) {
 #pragma unroll
               for (int t = 0; t < S; ++t) z2[t] = __dadd_rn(z2[t], __dmul_rn(sc.scoef[4], v[t]));
@@ -1555,10 +1695,12 @@ __global__ void __launch_bounds__(kCsThreads, 1)
           }
         }
       }
+#if !SK_CS_TMA
       // group G(y): U_{k-1} line y + 5, U_{k-2} line y + 4 (complete at step y + 4)
       if (nslot) copy_a(y + 5);
       if (compute) copy_b(y + 4);
       cs_commit();
+#endif
     } else {
       // reducer warps (R1 lane order): self-Gram of line y-1, raw Grams of line y-2
       const int r = warp - kCsColWarps - 1;
@@ -2935,7 +3077,7 @@ struct Launch {
     if constexpr (S <= 2) {
       const SideConst& sc = c.side[side0];
       const int nr = cols_ranges(sc, nz);
-      const size_t smem = sizeof(double) * ((kCsAR * kCsA + (kCsBR + kCsKR) * kCsK + 2 * kSeg) * S);
+      const size_t smem = sizeof(double) * ((kCsAR * kCsA + kCsBR * (SK_CS_TMA ? kCsA : kCsK) + kCsKR * kCsK + 2 * kSeg) * S);
       static bool attr = false;
       if (!attr) {
         cudaFuncSetAttribute(k_lanczos_cols<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
