@@ -735,9 +735,21 @@ __device__ inline bool gram_setup(const SolveConst& c, int side, int mode, const
   return false;
 }
 
+// Output halves per block: for S = 8 the 64 accumulators plus four rows of
+// operands in flight took 254 registers (8 warps per SM, 2.3 TB/s at config 4);
+// two CTAs per (block, row range), each owning half of the u index (32
+// accumulators, two rows in flight, 2 CTAs per SM), adjacent in launch order so
+// the second read of U_b's rows hits L2. Every entry keeps its R1 order.
 template <int S>
-__global__ void __launch_bounds__(256) k_gram(const __grid_constant__ SolveConst c, int mode) {
+struct GramSplit {
+  static constexpr int H = S >= 8 ? 2 : 1;
+  static constexpr int UNR = H == 2 ? 2 : 4;
+  static constexpr int MINB = H == 2 ? 2 : (S <= 4 ? 3 : 1);  // CTAs per SM (register budget)
+};
+template <int S>
+__global__ void __launch_bounds__(256, GramSplit<S>::MINB) k_gram(const __grid_constant__ SolveConst c, int mode) {
   constexpr int NB = S * S;
+  constexpr int H = GramSplit<S>::H, SU = S / H, NH = SU * S, UNR = GramSplit<S>::UNR;
   const int side = blockIdx.z;
   if (side >= c.nsides) return;
   const double* x;
@@ -749,7 +761,8 @@ __global__ void __launch_bounds__(256) k_gram(const __grid_constant__ SolveConst
   // grid x runs over the blocks, y over row ranges: the CTAs that are resident
   // together share a row range, so x's rows stay in L2 across all blocks (one
   // HBM read of x per pass instead of one per block)
-  const int64_t by = blockIdx.x;
+  const int64_t by = blockIdx.x / H;
+  const int h = (int)(blockIdx.x % H);
   if (by >= nblk) return;
   const int64_t cta = blockIdx.y;
   if (cta >= sc.ncta) return;
@@ -758,36 +771,46 @@ __global__ void __launch_bounds__(256) k_gram(const __grid_constant__ SolveConst
   const int lane = threadIdx.x & 31;
   const int64_t n = sc.n;
   const SegGeom g = seg_geom(cta, sc.nseg);
-  double* part = sc.part + ((by * sc.ncta + cta) * NB);
-  OwnerVals<NB> segv[kSegsPerWarp];
+  double* part = sc.part + ((by * sc.ncta + cta) * NB) + h * NH;  // entries u*S+t, u in this half
+  OwnerVals<NH> segv[kSegsPerWarp];
 #pragma unroll
   for (int q = 0; q < kSegsPerWarp; ++q) {
-    double acc[NB];
+    double acc[NH];
 #pragma unroll
-    for (int e = 0; e < NB; ++e) acc[e] = 0.0;
+    for (int e = 0; e < NH; ++e) acc[e] = 0.0;
     if (q < g.nvalid_warp) {
       const int64_t base = (g.seg_w0 + q) * kSeg;
-#pragma unroll 4
+#pragma unroll UNR
       for (int m = 0; m < kLRows; ++m) {
         const int64_t i = base + lane + 32 * m;
         if (i < n) {
-          double a[S], y[S];
+          double a[S], y[SU];
           ld_raw<S>(ub, i, a);
-          ld_raw<S>(x, i, y);
+          if constexpr (H == 1) {
+            ld_raw<S>(x, i, y);
+          } else {
+            const double2* py = reinterpret_cast<const double2*>(x + i * S + h * SU);
 #pragma unroll
-          for (int u = 0; u < S; ++u)
+            for (int u = 0; u < SU / 2; ++u) {
+              const double2 v = __ldg(py + u);
+              y[2 * u] = v.x;
+              y[2 * u + 1] = v.y;
+            }
+          }
+#pragma unroll
+          for (int u = 0; u < SU; ++u)
 #pragma unroll
             for (int t = 0; t < S; ++t)
               acc[u * S + t] = __dadd_rn(acc[u * S + t], __dmul_rn(a[t], y[u]));
         }
       }
     }
-    seg_butterfly<NB>(acc, segv[q], lane);
+    seg_butterfly<NH>(acc, segv[q], lane);
   }
-  cta_combine<NB>(segv, g.nvalid_warp, g.nvalid_cta, part);
+  cta_combine<NH>(segv, g.nvalid_warp, g.nvalid_cta, part);
 
   unsigned int* ctr = sc.counter;  // slots: 0 pass 1, 1 update, 2 clean-up, 4.. per block
-  if (!last_cta_arrive(ctr + 4 + by, (unsigned)sc.ncta)) return;
+  if (!last_cta_arrive(ctr + 4 + by, (unsigned)(sc.ncta * H))) return;
   __shared__ double G[NB];
   for (int e = threadIdx.x; e < NB; e += blockDim.x)
     G[e] = tree_stream(sc.part + by * sc.ncta * NB + e, sc.ncta, NB);
@@ -2975,7 +2998,8 @@ struct Launch {
   static void gram(const SolveConst& c, int mode, int64_t nblk, cudaStream_t st) {
     int64_t nmax, cmax;
     dims(c, nmax, cmax);
-    k_gram<S><<<dim3((unsigned)(nblk > 0 ? nblk : 1), (unsigned)cmax, c.nsides), 256, 0, st>>>(c, mode);
+    k_gram<S><<<dim3((unsigned)((nblk > 0 ? nblk : 1) * GramSplit<S>::H), (unsigned)cmax, c.nsides), 256, 0, st>>>(
+        c, mode);
   }
   static void update(const SolveConst& c, int mode, cudaStream_t st) {
     int64_t nmax, cmax;

@@ -206,6 +206,19 @@ def test_bicgstab_convdiff_bitwise(sk, po, s):
     _compare(sol, ref)
 
 
+@pytest.mark.parametrize("s", [6, 8])
+def test_bicgstab_wide_blocks_bitwise(sk, po, s):
+    """Config-4 block widths (s = 8: the split-output Arnoldi Gram, k_gram halves) on a
+    ragged row count (1728 = 3.375 R1 segments)."""
+    a = po.convection_diffusion_3d(12, (5.0, 2.5, 1.25))
+    b = po.laplacian_2d(40)
+    c1, c2 = po.random_rhs(a.n_rows, s, 7), po.random_rhs(b.n_rows, s, 8)
+    cfg = po.Config(eps_tol=1e-8, max_iter=12)
+    ref = po.factorized_bicgstab(a, b, c1, c2, cfg, po.REPRODUCIBLE)
+    sol = sk.factorized_bicgstab(to_sk(sk, a), to_sk(sk, b), c1, c2, sk.SolverConfig(eps_tol=1e-8, max_iter=12))
+    _compare(sol, ref)
+
+
 def test_bicgstab_config2_shape_first_iterations(sk, po):
     """BASELINE config 2 operators (2D convection-diffusion 256^2, Pe 10, winds (1,1)/(1,-1)),
     s = 4, first 6 iterations bitwise against the oracle."""
