@@ -1138,13 +1138,7 @@ struct Solver {
     SideBuf& b = side[sd];
     if ((int64_t)b.blocks.size() >= need) return;
     if (need > b.cap_blocks) throw SkError(SK_ERR_CAPACITY, "basis capacity exceeded");
-    // ghost rows on both sides (row partition); SK_BLOCK_STAGGER (bytes, multiple of
-    // 16) pads each block so that blocks do not sit a power of two apart
-    static const int64_t stagger = [] {
-      const char* e = getenv("SK_BLOCK_STAGGER");
-      return e ? (std::max<int64_t>(0, atoll(e)) / 16) * 2 : (int64_t)0;
-    }();
-    const int64_t stride = (b.n + 2 * b.halo) * s + stagger;
+    const int64_t stride = (b.n + 2 * b.halo) * s;  // ghost rows on both sides (row partition)
     const int64_t bb = stride * (int64_t)sizeof(double);
     int64_t per = std::max<int64_t>(1, (int64_t(1) << 30) / std::max<int64_t>(bb, 1));
     per = std::min<int64_t>(per, b.cap_blocks - (int64_t)b.blocks.size());
