@@ -203,6 +203,11 @@ sk_status sk_gen_stencil(int32_t kind, int64_t grid, const double* wind, int64_t
 /* random_rhs: rows x s column-major, std::mt19937_64 + Box-Muller (bitwise the reference's). */
 sk_status sk_gen_random_rhs(int64_t rows, int64_t s, uint64_t seed, double* out);
 
+/* Page-locked host buffers for inputs: C1 / C2 passed from such memory are copied
+ * by DMA directly (pageable memory goes through the library's pinned staging lanes). */
+sk_status sk_host_alloc(int64_t bytes, void** out);
+void sk_host_free(void* p);
+
 /* On-disk formats. Text is byte-identical to the reference's
  * writers (17 significant digits, "%.17g"); all return SK_ERR_IO on a failed
  * open or write, with the path in sk_last_error().

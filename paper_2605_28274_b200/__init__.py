@@ -568,6 +568,31 @@ def solve_local_group(method: str, a: SparseMatrix, b: Optional[SparseMatrix], c
     return sols
 
 
+# ---- page-locked host arrays ----
+class _Pinned:
+    def __init__(self, ptr):
+        self.ptr = ptr
+
+    def __del__(self):
+        try:
+            lib().sk_host_free(self.ptr)
+        except Exception:
+            pass
+
+
+def pinned_empty(shape, dtype=np.float64, order: str = "F") -> np.ndarray:
+    """A numpy array in page-locked host memory (sk_host_alloc): solver inputs in
+    such memory reach HBM by direct DMA instead of through the staging lanes."""
+    dt = np.dtype(dtype)
+    nbytes = int(np.prod(shape)) * dt.itemsize
+    p = C.c_void_p()
+    _check(lib().sk_host_alloc(C.c_int64(nbytes), C.byref(p)))
+    owner = _Pinned(p)
+    buf = (C.c_char * max(nbytes, 1)).from_address(p.value)
+    buf.owner = owner  # freed when the last view of the buffer goes away
+    return np.ndarray(shape, dtype=dt, buffer=buf, order=order)
+
+
 # ---- on-disk formats (SURVEY 8f-2; matrix_market.cpp, bench.cpp:179-193, main.cpp:146-239) ----
 def write_matrix_market(m, path: str) -> None:
     """write_matrix_market (matrix_market.cpp:148-175): a SparseMatrix as

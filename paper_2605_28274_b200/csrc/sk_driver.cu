@@ -455,6 +455,16 @@ void h2d_staged(void* dst, const void* src, size_t bytes, cudaStream_t st) {
   static std::mutex mu;
   static Lane lanes[kMaxLanes];
   static int dev_init = -1;
+  {
+    // caller memory that is already page-locked (sk_host_alloc, cudaHostAlloc,
+    // cudaHostRegister) goes straight to the DMA engine, no staging
+    cudaPointerAttributes pa;
+    if (cudaPointerGetAttributes(&pa, src) == cudaSuccess && pa.type == cudaMemoryTypeHost) {
+      CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, st));
+      return;
+    }
+    cudaGetLastError();
+  }
   std::lock_guard<std::mutex> g(mu);
   int dev = 0;
   CK(cudaGetDevice(&dev));
@@ -2346,6 +2356,22 @@ sk_status sk_solution_copy_W_cols(const sk_solution* sol, int64_t col0, int64_t 
   return copy_basis_cols(sol, sol->wblocks, sol->wnfac, sol->m, sol->rw, col0, ncols, out);
 }
 void sk_internal_set_error(const char* msg) { g_err = msg; }
+sk_status sk_host_alloc(int64_t bytes, void** out) {
+  if (!out || bytes < 0) {
+    g_err = "sk_host_alloc: bad arguments";
+    return SK_ERR_DIMENSION;
+  }
+  *out = nullptr;
+  if (cudaHostAlloc(out, (size_t)std::max<int64_t>(bytes, 1), cudaHostAllocDefault) != cudaSuccess) {
+    cudaGetLastError();
+    g_err = "sk_host_alloc: cudaHostAlloc failed";
+    return SK_ERR_OUT_OF_MEMORY;
+  }
+  return SK_OK;
+}
+void sk_host_free(void* p) {
+  if (p) cudaFreeHost(p);
+}
 sk_status sk_solution_copy_V(const sk_solution* sol, double* out) {
   return copy_basis(sol, sol->vblocks, sol->vnfac, sol->n, sol->rv, out);
 }

@@ -280,3 +280,19 @@ def test_speculative_stencil_invalid_row_raises(sk, po):
     a = sk.SparseMatrix(n, n, rp, ci, val)
     with pytest.raises(sk.InvalidMatrixError, match="strictly increasing"):
         sk.factorized_cg(a, a, po.random_dense(n, 1, 1), po.random_dense(n, 1, 2))
+
+
+def test_pinned_inputs_bitwise(sk, po):
+    """C1/C2 in page-locked memory (direct DMA) give the same bits as pageable inputs
+    (staging lanes)."""
+    a = po.laplacian_2d(48)
+    c1, c2 = po.random_rhs(a.n_rows, 2, 21), po.random_rhs(a.n_rows, 2, 22)
+    A = to_sk(sk, a)
+    p1, p2 = sk.pinned_empty(c1.shape), sk.pinned_empty(c2.shape)
+    p1[...] = c1
+    p2[...] = c2
+    cfg = sk.SolverConfig(eps_tol=1e-8)
+    s0 = sk.factorized_cg(A, A, c1, c2, cfg)
+    s1 = sk.factorized_cg(A, A, p1, p2, cfg)
+    assert np.array_equal(s0.history.rel_residuals(), s1.history.rel_residuals())
+    assert np.array_equal(s0.core, s1.core)
