@@ -36,13 +36,26 @@ class _Cfg(C.Structure):
 
 
 def build(force: bool = False) -> str:
-    if force or not os.path.exists(LIB_PATH) or os.path.getmtime(LIB_PATH) < os.path.getmtime(
-            os.path.join(HERE, "sk_oracle.c")):
+    src = max(os.path.getmtime(os.path.join(HERE, f)) for f in ("sk_oracle.c", "sk_oracle.h", "Makefile"))
+    if force or any(not os.path.exists(p) or os.path.getmtime(p) < src
+                    for p in (LIB_PATH, os.path.join(HERE, "libsk_oracle_mt.so"))):
         subprocess.check_call(["make", "-s", "-C", HERE])
     return LIB_PATH
 
 
 _lib = None
+
+
+def use_threads(threads: int) -> None:
+    """Switch to the OpenMP build (bitwise equal to the serial one) with `threads`
+    host threads for the oracle's loops and its SpMM (parallel.cpp's knob).
+    Golden generation only: the CPU baseline times the serial reference flags."""
+    global _lib, LIB_PATH
+    build()
+    os.environ["OMP_NUM_THREADS"] = str(threads)
+    LIB_PATH = os.path.join(HERE, "libsk_oracle_mt.so")
+    _lib = None
+    lib().sko_set_parallel(1, int(threads))
 
 
 def lib():
@@ -339,7 +352,9 @@ class Config:
 
 
 def solve(method: int, a: Csr, b: Csr | None, c1: np.ndarray, c2: np.ndarray | None,
-          cfg: Config | None = None, mode: int = REPRODUCIBLE) -> Solution:
+          cfg: Config | None = None, mode: int = REPRODUCIBLE, lean: bool = False) -> Solution:
+    """lean: Lanczos bases keep only their last blocks (history and core only; V, W
+    are returned empty) -- golden generation at configs larger than host RAM."""
     cfg = cfg or Config()
     c1 = np.asfortranarray(c1, dtype=np.float64)
     s = c1.shape[1]
@@ -353,10 +368,16 @@ def solve(method: int, a: Csr, b: Csr | None, c1: np.ndarray, c2: np.ndarray | N
         raise OracleError(-1, "DimensionError: factorized_cg_lyapunov: C1 rows must match A")
     h = C.c_void_p()
     cc = cfg.c()
-    _check(lib().sko_solve(int(method), C.byref(ca), C.byref(cb) if cb is not None else None,
+    L = lib()
+    if lean:
+        L.sko_set_lean(1)
+    try:
+        _check(L.sko_solve(int(method), C.byref(ca), C.byref(cb) if cb is not None else None,
                            _p(c1), _p(c2a) if c2a is not None else None, C.c_int64(s),
                            C.byref(cc), int(mode), C.byref(h)))
-    L = lib()
+    finally:
+        if lean:
+            L.sko_set_lean(0)
     try:
         nrec = int(L.sko_solution_n_records(h))
         it = np.zeros(nrec, dtype=np.int64)
@@ -366,9 +387,9 @@ def solve(method: int, a: Csr, b: Csr | None, c1: np.ndarray, c2: np.ndarray | N
         L.sko_solution_history(h, _p(it, i64p), _p(rel), _p(tb), _p(tk))
         n, rv, m, rw = (C.c_int64() for _ in range(4))
         L.sko_solution_dims(h, C.byref(n), C.byref(rv), C.byref(m), C.byref(rw))
-        V = np.zeros((n.value, rv.value), order="F")
+        V = np.zeros((n.value, 0 if lean else rv.value), order="F")
         core = np.zeros((rv.value, rw.value), order="F")
-        W = np.zeros((m.value, rw.value), order="F")
+        W = np.zeros((m.value, 0 if lean else rw.value), order="F")
         L.sko_solution_copy(h, _p(V), _p(core), _p(W))
         caps = []
         for i in range(int(L.sko_solution_n_captured(h))):
@@ -386,12 +407,12 @@ def solve(method: int, a: Csr, b: Csr | None, c1: np.ndarray, c2: np.ndarray | N
         L.sko_solution_free(h)
 
 
-def factorized_cg(a, b, c1, c2, cfg=None, mode=REPRODUCIBLE):
-    return solve(CG, a, b, c1, c2, cfg, mode)
+def factorized_cg(a, b, c1, c2, cfg=None, mode=REPRODUCIBLE, lean=False):
+    return solve(CG, a, b, c1, c2, cfg, mode, lean)
 
 
-def factorized_cg_lyapunov(a, c1, cfg=None, mode=REPRODUCIBLE):
-    return solve(CG_LYAPUNOV, a, None, c1, None, cfg, mode)
+def factorized_cg_lyapunov(a, c1, cfg=None, mode=REPRODUCIBLE, lean=False):
+    return solve(CG_LYAPUNOV, a, None, c1, None, cfg, mode, lean)
 
 
 def factorized_bicgstab(a, b, c1, c2, cfg=None, mode=REPRODUCIBLE):

@@ -25,6 +25,26 @@
 #define R2_TILE 32
 #define HH_RATIO 1e-6      /* sigma_min/sigma_max below this -> Householder path */
 
+/* Golden-generation build (libsk_oracle_mt.so, -fopenmp): loops over independent
+ * outputs run on all host threads. Every output keeps its own operation sequence,
+ * so results are bitwise those of the serial build (tests/test_oracle_pins.py
+ * checks both builds against the same fixtures). The default build (the CPU
+ * baseline) has no OpenMP, like the reference (proj/CMakeLists.txt:3-15). */
+#ifdef _OPENMP
+#define SKO_STR(x) #x
+#define SKO_PAR(cond) _Pragma(SKO_STR(omp parallel for schedule(static) if(cond)))
+#else
+#define SKO_PAR(cond)
+#endif
+#define PAR_MIN 4096 /* elements below which a loop stays serial */
+
+/* Lean Lanczos storage (golden generation at configs whose bases exceed host RAM):
+ * only the last LEAN_KEEP blocks are kept; a clean-up pass (which needs every block)
+ * or a request for V fails loudly instead. */
+#define LEAN_KEEP 3
+static int g_lean = 0;
+void sko_set_lean(int on) { g_lean = on; }
+
 static __thread char g_err[512];
 static void set_err(const char* fmt, ...) {
     va_list ap;
@@ -90,6 +110,7 @@ static dmat dm_embed(const dmat* x, int64_t rows, int64_t cols) {
 /* axpy (dense_matrix.cpp:105-108): y += alpha * x, mul then add per entry. */
 static void dm_axpy(double alpha, const dmat* x, dmat* y) {
     const size_t n = (size_t)(x->rows * x->cols);
+    SKO_PAR(n >= PAR_MIN)
     for (size_t i = 0; i < n; ++i) y->a[i] = y->a[i] + alpha * x->a[i];
 }
 /* matmul_a_bt (dense_matrix.cpp:124-129): out(i,j) = sum_t a(i,t) b(j,t). */
@@ -131,8 +152,9 @@ static double r1_dot(const double* x, const double* y, int64_t n, int64_t row0) 
     if (n <= 0) return 0.0;
     const int64_t S = (n + R1_SEG - 1) / R1_SEG;
     double* seg = (double*)xcalloc((size_t)S, sizeof(double));
-    double lane[R1_LANES];
+    SKO_PAR(S >= 64)
     for (int64_t g = 0; g < S; ++g) {
+        double lane[R1_LANES];
         for (int l = 0; l < R1_LANES; ++l) {
             double acc = 0.0;
             for (int m = 0; m < R1_LROWS; ++m) {
@@ -160,9 +182,11 @@ static double r2_inner(const dmat* a, const dmat* b, int64_t rows, int64_t cols)
     if (rows <= 0 || cols <= 0) return 0.0;
     const int64_t nti = (rows + R2_TILE - 1) / R2_TILE, ntj = (cols + R2_TILE - 1) / R2_TILE;
     double* colres = (double*)xcalloc((size_t)ntj, sizeof(double));
-    double* tiles = (double*)xcalloc((size_t)nti, sizeof(double));
-    double lane[R1_LANES];
+    double* tiles_all = (double*)xcalloc((size_t)(nti * ntj), sizeof(double));
+    SKO_PAR(ntj >= 8)
     for (int64_t tj = 0; tj < ntj; ++tj) {
+        double lane[R1_LANES];
+        double* tiles = tiles_all + tj * nti;
         for (int64_t ti = 0; ti < nti; ++ti) {
             for (int l = 0; l < R1_LANES; ++l) {
                 const int64_t i = ti * R2_TILE + l;
@@ -181,7 +205,7 @@ static double r2_inner(const dmat* a, const dmat* b, int64_t rows, int64_t cols)
     }
     const double r = tree_reduce(colres, ntj);
     free(colres);
-    free(tiles);
+    free(tiles_all);
     return r;
 }
 /* frobenius_inner / windowed_inner (dense_matrix.cpp:131-152): sequential. */
@@ -730,19 +754,24 @@ static void householder_qr(const double* x, int64_t n, int64_t s, dot_fn dot, do
         const double t = -v0 / alpha;
         tau[j] = t;
         const int64_t tail = n - j - 1;
-        if (tail > 0)
+        if (tail > 0) {
+            SKO_PAR(tail >= PAR_MIN)
             for (int64_t i = j + 1; i < n; ++i) W(i, j) = W(i, j) / v0;
+        }
         const int64_t rest = s - j - 1;
         if (rest > 0) {
+            SKO_PAR(rest > 1 && tail >= PAR_MIN)
             for (int64_t c = j + 1; c < s; ++c) {
                 double pr = W(j, c);
                 if (tail > 0) pr = pr + dot(&W(0, j), &W(0, c), n, j + 1);
                 proj[c] = pr * t;
             }
             for (int64_t c = j + 1; c < s; ++c) W(j, c) = W(j, c) - proj[c];
-            if (tail > 0)
-                for (int64_t c = j + 1; c < s; ++c)
-                    for (int64_t i = j + 1; i < n; ++i) W(i, c) = W(i, c) - W(i, j) * proj[c];
+            if (tail > 0) {
+                SKO_PAR(tail >= PAR_MIN)
+                for (int64_t i = j + 1; i < n; ++i)
+                    for (int64_t c = j + 1; c < s; ++c) W(i, c) = W(i, c) - W(i, j) * proj[c];
+            }
         }
     }
     double* q = qout;
@@ -753,15 +782,18 @@ static void householder_qr(const double* x, int64_t n, int64_t s, dot_fn dot, do
         const double t = tau[j];
         if (t == 0.0) continue;
         const int64_t tail = n - j - 1;
+        SKO_PAR(p - j > 1 && tail >= PAR_MIN)
         for (int64_t c = j; c < p; ++c) {
             double pr = Q(j, c);
             if (tail > 0) pr = pr + dot(&W(0, j), &Q(0, c), n, j + 1);
             proj[c] = pr * t;
         }
         for (int64_t c = j; c < p; ++c) Q(j, c) = Q(j, c) - proj[c];
-        if (tail > 0)
-            for (int64_t c = j; c < p; ++c)
-                for (int64_t i = j + 1; i < n; ++i) Q(i, c) = Q(i, c) - W(i, j) * proj[c];
+        if (tail > 0) {
+            SKO_PAR(tail >= PAR_MIN)
+            for (int64_t i = j + 1; i < n; ++i)
+                for (int64_t c = j; c < p; ++c) Q(i, c) = Q(i, c) - W(i, j) * proj[c];
+        }
     }
     memset(rout, 0, sizeof(double) * (size_t)(p * s));
     for (int64_t j = 0; j < s; ++j)
@@ -769,6 +801,7 @@ static void householder_qr(const double* x, int64_t n, int64_t s, dot_fn dot, do
     for (int64_t j = 0; j < p; ++j)
         if (rout[j * p + j] < 0.0) {
             for (int64_t c = j; c < s; ++c) rout[c * p + j] = -rout[c * p + j];
+            SKO_PAR(n >= PAR_MIN)
             for (int64_t i = 0; i < n; ++i) Q(i, j) = -Q(i, j);
         }
 #undef W
@@ -803,27 +836,36 @@ struct sko_basis {
     int64_t steps, hcap;
     double hfro2;
     int exhausted, broken;
+    int lean; /* keep only the last LEAN_KEEP blocks (Lanczos, golden generation) */
     int64_t paths[4];
 };
 
-static double* blk(const sko_basis* b, int64_t j) { return b->v + (size_t)(j * b->s * b->n); }
-static double* ublk(const sko_basis* b, int64_t j) { return b->u + (size_t)(j * b->s * b->n); }
+/* Reference order stores the orthonormal blocks V; the reproducible contract stores
+ * only the raw blocks U_b and their factors N_b (V_b = U_b N_b^{-1} is formed on
+ * output, bitwise the block the extension produced). */
+static int64_t slot(const sko_basis* b, int64_t j) { return b->lean ? j % LEAN_KEEP : j; }
+static double* blk(const sko_basis* b, int64_t j) { return b->v + (size_t)(slot(b, j) * b->s * b->n); }
+static double* ublk(const sko_basis* b, int64_t j) { return b->u + (size_t)(slot(b, j) * b->s * b->n); }
 static double* nfb(const sko_basis* b, int64_t j) { return b->nf + (size_t)(j * b->s * b->s); }
 
 /* q: orthonormal block; u/N: its raw form and factor (reproducible mode only) */
 static void basis_append(sko_basis* b, const double* q, const double* u, const double* N) {
     if (b->blocks == b->cap) {
-        b->cap = b->cap ? 2 * b->cap : 8;
-        b->v = (double*)realloc(b->v, sizeof(double) * (size_t)(b->cap * b->s * b->n));
-        if (!b->v) abort();
-        if (b->mode == SKO_REPRODUCIBLE) {
-            b->u = (double*)realloc(b->u, sizeof(double) * (size_t)(b->cap * b->s * b->n));
-            b->nf = (double*)realloc(b->nf, sizeof(double) * (size_t)(b->cap * b->s * b->s));
+        const int64_t ncap = b->cap ? 2 * b->cap : 8;
+        const int64_t dcap = b->lean ? LEAN_KEEP : ncap; /* n x s data slots */
+        if (b->mode == SKO_REFERENCE_ORDER) {
+            b->v = (double*)realloc(b->v, sizeof(double) * (size_t)(dcap * b->s * b->n));
+            if (!b->v) abort();
+        } else {
+            b->u = (double*)realloc(b->u, sizeof(double) * (size_t)(dcap * b->s * b->n));
+            b->nf = (double*)realloc(b->nf, sizeof(double) * (size_t)(ncap * b->s * b->s));
             if (!b->u || !b->nf) abort();
         }
+        b->cap = ncap;
     }
-    memcpy(blk(b, b->blocks), q, sizeof(double) * (size_t)(b->s * b->n));
-    if (b->mode == SKO_REPRODUCIBLE) {
+    if (b->mode == SKO_REFERENCE_ORDER) {
+        memcpy(blk(b, b->blocks), q, sizeof(double) * (size_t)(b->s * b->n));
+    } else {
         memcpy(ublk(b, b->blocks), u, sizeof(double) * (size_t)(b->s * b->n));
         memcpy(nfb(b, b->blocks), N, sizeof(double) * (size_t)(b->s * b->s));
     }
@@ -850,18 +892,48 @@ static void basis_apply(const sko_basis* b, const double* x, double* y) {
         sko_spmm(&b->opT, x, b->s, y); /* gather in ascending source row == scatter order */
 }
 
-/* X^T Y (s x s) with the mode's reduction: out[u*s+t] = sum_i X(i,t) Y(i,u). */
+/* X^T Y (s x s) with the mode's reduction: out[u*s+t] = sum_i X(i,t) Y(i,u).
+ * Reference order: one sequential dot per entry. Reproducible: every entry's R1
+ * sum (r1_dot), all entries formed segment by segment. */
 static void gram(const sko_basis* b, const double* X, const double* Y, double* out) {
-    const int64_t n = b->n, s = b->s;
-    dot_fn dot = b->mode == SKO_REPRODUCIBLE ? r1_dot : seq_dot;
-    for (int64_t u = 0; u < s; ++u)
-        for (int64_t t = 0; t < s; ++t) out[u * s + t] = dot(X + t * n, Y + u * n, n, 0);
+    const int64_t n = b->n, s = b->s, ss = s * s;
+    if (b->mode != SKO_REPRODUCIBLE) {
+        SKO_PAR(ss > 1 && n >= PAR_MIN)
+        for (int64_t e = 0; e < ss; ++e) {
+            const int64_t u = e / s, t = e % s;
+            out[u * s + t] = seq_dot(X + t * n, Y + u * n, n, 0);
+        }
+        return;
+    }
+    const int64_t S = (n + R1_SEG - 1) / R1_SEG;
+    double* seg = (double*)xcalloc((size_t)(S * ss), sizeof(double));
+    SKO_PAR(S >= 16)
+    for (int64_t g = 0; g < S; ++g) {
+        double lane[R1_LANES];
+        for (int64_t e = 0; e < ss; ++e) {
+            const double* x = X + (e % s) * n;
+            const double* y = Y + (e / s) * n;
+            for (int l = 0; l < R1_LANES; ++l) {
+                double acc = 0.0;
+                for (int m = 0; m < R1_LROWS; ++m) {
+                    const int64_t i = g * R1_SEG + l + R1_LANES * m;
+                    if (i < n) acc = acc + x[i] * y[i];
+                }
+                lane[l] = acc;
+            }
+            butterfly32(lane);
+            seg[e * S + g] = lane[0];
+        }
+    }
+    for (int64_t e = 0; e < ss; ++e) out[(e / s) * s + (e % s)] = tree_reduce(seg + e * S, S);
+    free(seg);
 }
 /* w -= V c per row: tmp = sum_t V(i,t) c(t,u) (sequential), w = w - tmp. */
 static void sub_vc(const sko_basis* b, const double* V, const double* c, double* w) {
     const int64_t n = b->n, s = b->s;
-    for (int64_t u = 0; u < s; ++u)
-        for (int64_t i = 0; i < n; ++i) {
+    SKO_PAR(n >= PAR_MIN)
+    for (int64_t i = 0; i < n; ++i)
+        for (int64_t u = 0; u < s; ++u) {
             double tmp = 0.0;
             for (int64_t t = 0; t < s; ++t) tmp = tmp + V[t * n + i] * c[u * s + t];
             w[u * n + i] = w[u * n + i] - tmp;
@@ -874,6 +946,7 @@ static void apply_norm(const sko_basis* b, const double* w, const double* N, dou
     const int64_t n = b->n, s = b->s;
     double dinv[64];
     for (int64_t u = 0; u < s; ++u) dinv[u] = 1.0 / N[u * s + u];
+    SKO_PAR(n >= PAR_MIN)
     for (int64_t i = 0; i < n; ++i)
         for (int64_t u = 0; u < s; ++u) {
             double acc = w[u * n + i];
@@ -1006,6 +1079,7 @@ int sko_basis_init(const sko_csr* op, const double* start, int64_t s, int arnold
     b->tol = breakdown_tol;
     b->n = op->n_rows;
     b->s = s;
+    b->lean = g_lean && !arnoldi && !lanczos_full_reorth;
     if (transpose && mode == SKO_REPRODUCIBLE) {
         sko_csr_transpose(op, &b->opT);
         b->has_opT = 1;
@@ -1144,6 +1218,10 @@ int sko_basis_try_extend(sko_basis* b) {
     const double scale = sqrt(b->hfro2 + coeff2 + r2);
 
     if (!b->arnoldi && smin < b->tol * scale) { /* :113-124 clean-up, not recorded in H */
+        if (b->lean) {
+            free(w); free(wr); free(hcoef); free(q); free(uk);
+            return set_err("lean basis: a clean-up pass needs every block"), SKO_ERR_ALLOC;
+        }
         if (b->mode == SKO_REFERENCE_ORDER) {
             double c[64 * 64];
             for (int64_t jb = 0; jb < k; ++jb) {
@@ -1205,9 +1283,19 @@ int sko_basis_try_extend(sko_basis* b) {
 int64_t sko_basis_cols(const sko_basis* b) { return b->blocks * b->s; }
 int64_t sko_basis_steps(const sko_basis* b) { return b->steps; }
 int sko_basis_exhausted(const sko_basis* b) { return b->exhausted; }
-void sko_basis_matrix(const sko_basis* b, double* out) {
-    memcpy(out, b->v, sizeof(double) * (size_t)(b->blocks * b->s * b->n));
+/* the first `blocks` blocks of V, column-major (basis_prefix, block_krylov.cpp:152-157) */
+static int basis_v_out(const sko_basis* b, int64_t blocks, double* out) {
+    if (b->lean) return set_err("lean basis: V is not kept"), SKO_ERR_ALLOC;
+    const size_t bs = (size_t)(b->s * b->n);
+    for (int64_t j = 0; j < blocks; ++j) {
+        if (b->mode == SKO_REFERENCE_ORDER)
+            memcpy(out + j * bs, blk(b, j), sizeof(double) * bs);
+        else
+            apply_norm(b, ublk(b, j), nfb(b, j), out + j * bs);
+    }
+    return SKO_OK;
 }
+void sko_basis_matrix(const sko_basis* b, double* out) { basis_v_out(b, b->blocks, out); }
 void sko_basis_path_counts(const sko_basis* b, int64_t* out4) { memcpy(out4, b->paths, sizeof b->paths); }
 void sko_basis_free(sko_basis* b) {
     if (!b) return;
@@ -1241,38 +1329,42 @@ static double h_at(const sko_basis* b, int64_t i, int64_t l) {
 
 /* accumulate_h_times (block_krylov.cpp:173-192): c += H p, block by block,
  * each block's s-term dot formed first and then added (GEBP structure). */
+/* (Every output entry c(i,j) receives its block terms in ascending jb; the loops
+ * run output columns outermost so they can be spread over threads.) */
 static void acc_h_times(const sko_basis* b, const dmat* p, dmat* c) {
     const int64_t s = b->s, jblocks = p->rows / s;
-    for (int64_t jb = 0; jb < jblocks; ++jb) {
-        const int64_t r0 = b->arnoldi ? 0 : ((jb - 1) * s > 0 ? (jb - 1) * s : 0);
-        const int64_t r1 = b->hrows[jb] < c->rows ? b->hrows[jb] : c->rows;
-        if (r1 <= r0) continue;
-        const double* hb = b->hcol[jb];
-        const int64_t hr = b->hrows[jb];
-        for (int64_t j = 0; j < p->cols; ++j)
+    SKO_PAR(p->cols > 1 && p->cols * c->rows >= PAR_MIN)
+    for (int64_t j = 0; j < p->cols; ++j)
+        for (int64_t jb = 0; jb < jblocks; ++jb) {
+            const int64_t r0 = b->arnoldi ? 0 : ((jb - 1) * s > 0 ? (jb - 1) * s : 0);
+            const int64_t r1 = b->hrows[jb] < c->rows ? b->hrows[jb] : c->rows;
+            if (r1 <= r0) continue;
+            const double* hb = b->hcol[jb];
+            const int64_t hr = b->hrows[jb];
             for (int64_t i = r0; i < r1; ++i) {
                 double d = 0.0;
                 for (int64_t t = 0; t < s; ++t) d = d + hb[t * hr + i] * AT(*p, jb * s + t, j);
                 AT(*c, i, j) = AT(*c, i, j) + d;
             }
-    }
+        }
 }
 /* accumulate_times_ht (block_krylov.cpp:194-213): c += p H^T. */
 static void acc_times_ht(const sko_basis* b, const dmat* p, dmat* c) {
     const int64_t s = b->s, jblocks = p->cols / s;
-    for (int64_t jb = 0; jb < jblocks; ++jb) {
-        const int64_t r0 = b->arnoldi ? 0 : ((jb - 1) * s > 0 ? (jb - 1) * s : 0);
-        const int64_t r1 = b->hrows[jb] < c->cols ? b->hrows[jb] : c->cols;
-        if (r1 <= r0) continue;
-        const double* hb = b->hcol[jb];
-        const int64_t hr = b->hrows[jb];
-        for (int64_t jc = r0; jc < r1; ++jc)
+    SKO_PAR(c->cols > 1 && c->cols * p->rows >= PAR_MIN)
+    for (int64_t jc = 0; jc < c->cols; ++jc)
+        for (int64_t jb = 0; jb < jblocks; ++jb) {
+            const int64_t r0 = b->arnoldi ? 0 : ((jb - 1) * s > 0 ? (jb - 1) * s : 0);
+            const int64_t r1 = b->hrows[jb] < c->cols ? b->hrows[jb] : c->cols;
+            if (jc < r0 || jc >= r1) continue;
+            const double* hb = b->hcol[jb];
+            const int64_t hr = b->hrows[jb];
             for (int64_t i = 0; i < p->rows; ++i) {
                 double d = 0.0;
                 for (int64_t t = 0; t < s; ++t) d = d + AT(*p, i, jb * s + t) * hb[t * hr + jc];
                 AT(*c, i, jc) = AT(*c, i, jc) + d;
             }
-    }
+        }
 }
 int sko_basis_accumulate_h_times(const sko_basis* b, const double* p, int64_t pr, int64_t pc,
                                  double* c, int64_t cr, int64_t cc) {
@@ -1291,6 +1383,25 @@ int sko_basis_accumulate_times_ht(const sko_basis* b, const double* p, int64_t p
     dmat P = {pr, pc, (double*)p}, C = {cr, cc, c};
     acc_times_ht(b, &P, &C);
     return SKO_OK;
+}
+
+/* acc[i] = fma(x[i], a, acc[i]) for i < n (one rounding per term; hardware FMA
+ * when the host has it -- bitwise the same result as libm's fma). */
+#if defined(__x86_64__) && defined(__GNUC__)
+__attribute__((target("avx2,fma"))) static void fma_axpy_hw(double* acc, const double* x, double a, int64_t n) {
+    for (int64_t i = 0; i < n; ++i) acc[i] = __builtin_fma(x[i], a, acc[i]);
+}
+#endif
+static void fma_axpy(double* acc, const double* x, double a, int64_t n) {
+#if defined(__x86_64__) && defined(__GNUC__)
+    static int hw = -1;
+    if (hw < 0) hw = __builtin_cpu_supports("fma") && __builtin_cpu_supports("avx2");
+    if (hw) {
+        fma_axpy_hw(acc, x, a, n);
+        return;
+    }
+#endif
+    for (int64_t i = 0; i < n; ++i) acc[i] = fma(x[i], a, acc[i]);
 }
 
 /* ------------------------------------------------------------------------- */
@@ -1323,24 +1434,28 @@ static dmat image(const sko_basis* vb, const sko_basis* wb, const dmat* p, int64
         acc_h_times(vb, p, &hpart);
         acc_times_ht(wb, p, &gpart);
     } else {
-        for (int64_t j = 0; j < p->cols && j < cols; ++j)
-            for (int64_t i = 0; i < rows; ++i) {
-                double acc = 0.0;
-                for (int64_t l = 0; l < p->rows; ++l) {
-                    if (i >= vb->hrows[l / vb->s]) continue; /* structural zero */
-                    acc = fma(h_at(vb, i, l), AT(*p, l, j), acc);
-                }
-                AT(hpart, i, j) = acc;
+        /* hpart(i,j) = fma chain over l ascending of H(i,l) p(l,j), structural zeros
+         * of the block Hessenberg skipped; gpart(i,j) likewise over p(i,l) G(j,l).
+         * Each entry's chain is formed in its own accumulator (column j at a time). */
+        const int64_t hc = p->cols < cols ? p->cols : cols;
+        SKO_PAR(hc > 1)
+        for (int64_t j = 0; j < hc; ++j) {
+            double* acc = &AT(hpart, 0, j);
+            for (int64_t l = 0; l < p->rows; ++l) {
+                const int64_t e = l / vb->s, hr = vb->hrows[e];
+                const int64_t lim = rows < hr ? rows : hr;
+                fma_axpy(acc, vb->hcol[e] + (l % vb->s) * hr, AT(*p, l, j), lim);
             }
-        for (int64_t j = 0; j < cols; ++j)
-            for (int64_t i = 0; i < p->rows && i < rows; ++i) {
-                double acc = 0.0;
-                for (int64_t l = 0; l < p->cols; ++l) {
-                    if (j >= wb->hrows[l / wb->s]) continue;
-                    acc = fma(AT(*p, i, l), h_at(wb, j, l), acc);
-                }
-                AT(gpart, i, j) = acc;
+        }
+        const int64_t gr = p->rows < rows ? p->rows : rows;
+        SKO_PAR(cols > 1)
+        for (int64_t j = 0; j < cols; ++j) {
+            double* acc = &AT(gpart, 0, j);
+            for (int64_t l = 0; l < p->cols; ++l) {
+                if (j >= wb->hrows[l / wb->s]) continue;
+                fma_axpy(acc, &AT(*p, 0, l), h_at(wb, j, l), gr);
             }
+        }
     }
     for (int64_t j = 0; j < cols; ++j)
         for (int64_t i = 0; i < rows; ++i) {
@@ -1398,10 +1513,12 @@ static void finish_solution(sko_solution* sol, const sko_basis* vb, const sko_ba
     sol->m = wb->n;
     sol->rv = x->rows;
     sol->rw = x->cols;
-    sol->V = (double*)xcalloc((size_t)(sol->n * sol->rv), sizeof(double));
-    sol->W = (double*)xcalloc((size_t)(sol->m * sol->rw), sizeof(double));
-    memcpy(sol->V, vb->v, sizeof(double) * (size_t)(sol->n * sol->rv));
-    memcpy(sol->W, wb->v, sizeof(double) * (size_t)(sol->m * sol->rw));
+    if (!vb->lean) { /* lean runs keep the history and the core only */
+        sol->V = (double*)xcalloc((size_t)(sol->n * sol->rv), sizeof(double));
+        sol->W = (double*)xcalloc((size_t)(sol->m * sol->rw), sizeof(double));
+        basis_v_out(vb, sol->rv / vb->s, sol->V);
+        basis_v_out(wb, sol->rw / wb->s, sol->W);
+    }
     sol->core = x->a;
     x->a = NULL;
     for (int i = 0; i < 4; ++i) sol->paths[i] = vb->paths[i] + (vb != wb ? wb->paths[i] : 0);
@@ -1703,9 +1820,9 @@ void sko_solution_dims(const sko_solution* sol, int64_t* n, int64_t* rv, int64_t
     *rw = sol->rw;
 }
 void sko_solution_copy(const sko_solution* sol, double* v, double* core, double* w) {
-    if (v) memcpy(v, sol->V, sizeof(double) * (size_t)(sol->n * sol->rv));
-    if (core) memcpy(core, sol->core, sizeof(double) * (size_t)(sol->rv * sol->rw));
-    if (w) memcpy(w, sol->W, sizeof(double) * (size_t)(sol->m * sol->rw));
+    if (v && sol->V) memcpy(v, sol->V, sizeof(double) * (size_t)(sol->n * sol->rv));
+    if (core && sol->core) memcpy(core, sol->core, sizeof(double) * (size_t)(sol->rv * sol->rw));
+    if (w && sol->W) memcpy(w, sol->W, sizeof(double) * (size_t)(sol->m * sol->rw));
 }
 int64_t sko_solution_n_captured(const sko_solution* sol) { return sol->ncap; }
 void sko_solution_captured(const sko_solution* sol, int64_t i, int64_t* rows, int64_t* cols, double* out) {

@@ -62,6 +62,7 @@ enum { SKO_METHOD_CG = 0, SKO_METHOD_CG_LYAPUNOV = 1, SKO_METHOD_BICGSTAB = 2 };
 
 const char* sko_last_error(void);
 int sko_contract_constants(int64_t* out4); /* {R1 segment rows, lanes, R2 tile, pyth guard bits} */
+void sko_set_lean(int on); /* golden generation: keep only the last Lanczos blocks (no V output) */
 
 /* ---- CSR / problems (sparse_matrix.cpp, problems.cpp) ---- */
 int sko_csr_from_triplets(int64_t n_rows, int64_t n_cols, int64_t count, const int64_t* rows,

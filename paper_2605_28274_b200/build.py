@@ -37,8 +37,23 @@ def units():
     return [(src, obj.replace(".o", OBJ_SUFFIX + ".o"), defs + EXTRA_DEFS) for src, obj, defs in u]
 
 
+if EXTRA_DEFS and not VARIANT:
+    raise RuntimeError("SK_DEFS builds an experiment variant: set SK_VARIANT=<name> too "
+                       "(the default libsk_b200.so is only built from the default flags)")
+
+
+def _flags_stamp() -> str:
+    import hashlib
+    return hashlib.sha256(" ".join(FLAGS + EXTRA_DEFS + [NVCC]).encode()).hexdigest()[:16]
+
+
 def needs_build() -> bool:
     if not os.path.exists(LIB):
+        return True
+    try:  # the flags a library was built with are stamped next to it
+        if open(LIB + ".flags").read().strip() != _flags_stamp():
+            return True
+    except OSError:
         return True
     t = os.path.getmtime(LIB)
     deps = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if not f.endswith(".o")]
@@ -76,6 +91,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     subprocess.check_call([NVCC, "-shared", *ARCH, *objs, "-o", LIB + ".tmp", "-lcudart", "-lcublas", "-lcusolver",
                            "-Xcompiler", "-pthread", "-ldl"])
     os.replace(LIB + ".tmp", LIB)
+    with open(LIB + ".flags", "w") as f:
+        f.write(_flags_stamp() + "\n")
     return LIB
 
 

@@ -339,9 +339,15 @@ bool detect_stencil(const int64_t* rp, const int64_t* ci, const double* val, int
 // on a helper thread while the device solves (SpecCtx). If that check fails, the
 // one-shot call discards its result and reruns the fully checked path, so
 // results and errors are those of the checked path.
+//
+// Nothing on the host may index an unvalidated row before the speculation is
+// settled: create_problem calls settle() before any check that walks the rows
+// (bitwise / tolerance symmetry, transpose); it joins the helper and, if a row
+// failed, re-runs the full validation synchronously (errors of the checked path).
 struct SpecCtx {
   std::vector<std::thread> th;
   std::atomic<bool> ok{true};
+  bool settled = false;
   void verify(const sk_csr* a, const StencilInfo& cand) {
     th.emplace_back([this, a, cand] {
       StencilInfo c = cand;
@@ -1699,10 +1705,31 @@ sk_problem* create_problem(int32_t method, const sk_csr* a, const sk_csr* b, con
   bool ab_same = false;
   // grid stencils are detected once, up front (a linear pass): a mirror-symmetric
   // stencil is bitwise symmetric without the per-entry search
-  auto sym_a = [&] { return stencil_symmetric(st_a) || bitwise_symmetric(a); };
+  // the speculated rows are checked before any host pass indexes them (see SpecCtx)
+  auto settle = [&] {
+    if (!spec || spec->settled) return;
+    const bool held = spec->join();
+    spec->settled = true;
+    spec->ok = true;  // from here on the problem is built from fully checked rows
+    if (held) return;
+    st_a = StencilInfo();
+    st_b = StencilInfo();
+    validate_detect(a, "A", use_st, st_a);
+    if (!lyap) {
+      if (same_csr(a, b))
+        st_b = st_a;
+      else
+        validate_detect(b, "B", use_st, st_b);
+    }
+  };
+  auto sym_a = [&] {
+    if (stencil_symmetric(st_a)) return true;
+    settle();
+    return stencil_symmetric(st_a) || bitwise_symmetric(a);
+  };
   if (lyap) {
     if (a->n_rows != a->n_cols) throw SkError(SK_ERR_DIMENSION, "factorized_cg_lyapunov: A must be square");
-    if (!sym_a() && !is_symmetric(a, 1e-12))
+    if (!sym_a() && (settle(), !is_symmetric(a, 1e-12)))
       throw SkError(SK_ERR_INVALID_MATRIX, "factorized_cg_lyapunov: A is not symmetric");
   } else {
     ab_same = same_csr(a, b);
@@ -1711,7 +1738,10 @@ sk_problem* create_problem(int32_t method, const sk_csr* a, const sk_csr* b, con
       throw SkError(SK_ERR_DIMENSION, "solver: A and B must be square");
     if (s < 1) throw SkError(SK_ERR_DIMENSION, "solver: C1 and C2 must have the same positive column count");
     if (ab_same) st_b = st_a;
-    if (stencil_symmetric(st_b) || bitwise_symmetric(b)) {
+    // BiCGSTAB on a detected stencil B applies B^T as the mirrored stencil (bitwise
+    // the transpose), so no host pass reads B's rows before the speculation settles
+    const bool mirror_ok = st_b.dim && method == SK_METHOD_BICGSTAB && !comm;
+    if (stencil_symmetric(st_b) || (!mirror_ok && (settle(), bitwise_symmetric(b)))) {
       bt_is_b = true;
     } else if (method == SK_METHOD_BICGSTAB && !comm && st_b.dim) {
       bt_mirror = true;  // B^T(i, i+o) = B(i+o, i): slot o takes B's value of slot -o
@@ -1719,13 +1749,15 @@ sk_problem* create_problem(int32_t method, const sk_csr* a, const sk_csr* b, con
       const int ns = bt_st.dim == 2 ? 5 : 7;
       for (int q = 0; q < ns; ++q) bt_st.c[q] = st_b.c[ns - 1 - q];
     } else {
+      settle();
       bt = transpose(b);
     }
     if (method == SK_METHOD_CG) {
-      const bool a_sym = (ab_same && bt_is_b) || (ab_same ? is_symmetric_with(a, bt, 1e-12)
-                                                          : (sym_a() || is_symmetric(a, 1e-12)));
+      const bool a_sym = (ab_same && bt_is_b) ||
+                         (ab_same ? (settle(), is_symmetric_with(a, bt, 1e-12))
+                                  : (sym_a() || (settle(), is_symmetric(a, 1e-12))));
       if (!a_sym) throw SkError(SK_ERR_INVALID_MATRIX, "factorized_cg: A is not symmetric");
-      if (!bt_is_b && !is_symmetric_with(b, bt, 1e-12))
+      if (!bt_is_b && (settle(), !is_symmetric_with(b, bt, 1e-12)))
         throw SkError(SK_ERR_INVALID_MATRIX, "factorized_cg: B is not symmetric");
     }
   }

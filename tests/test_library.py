@@ -159,3 +159,28 @@ def test_speculative_stencil_invalid_row_raises_without_device(skl):
     bad = skl.SparseMatrix(n, n, a.row_ptr, ci, a.values)
     with pytest.raises(skl.InvalidMatrixError, match="strictly increasing"):
         skl.factorized_cg(bad, bad, np.ones((n, 1)), np.ones((n, 1)))
+
+
+@pytest.mark.parametrize("method", ["cg", "bicgstab", "lyapunov"])
+def test_speculative_stencil_late_row_out_of_range(skl, method):
+    """a nonsymmetric stencil whose LAST row holds an out-of-range
+    column must raise InvalidMatrixError (sparse_matrix.cpp:12-32), not crash: the
+    speculative stencil path may not let a host pass (symmetry, transpose) index the
+    unvalidated rows. Runs without a device (host checks come first)."""
+    from paper_2605_28274_b200 import problems as pr
+    g = 64
+    n = g * g
+    for wind in ((10.0, 10.0), (0.0, 0.0)):
+        c = pr.convection_diffusion_2d(g, wind)
+        ci = np.array(c.col_idx, copy=True)
+        ci[-1] = 5000  # n = 4096
+        bad = skl.SparseMatrix(n, n, c.row_ptr, ci, c.values)
+        good = skl.SparseMatrix(n, n, c.row_ptr, c.col_idx, c.values)
+        c1, c2 = np.ones((n, 1)), np.ones((n, 1))
+        with pytest.raises(skl.InvalidMatrixError):
+            if method == "cg":
+                skl.factorized_cg(bad, bad, c1, c2)
+            elif method == "lyapunov":
+                skl.factorized_cg_lyapunov(bad, c1)
+            else:
+                skl.factorized_bicgstab(good, bad, c1, c2)
