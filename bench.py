@@ -50,10 +50,11 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--config", type=int, default=5)
-    ap.add_argument("--cpu-iters", type=int, default=2)
+    ap.add_argument("--cpu-iters", type=int, default=0, help="CPU sample length (default: 10 for cpu_baseline, 5 for --impl reference)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--no-factors", action="store_true", help="skip the e2e_with_factors leg (V, W copied to the host)")
     return ap.parse_args()
 
 
@@ -147,51 +148,89 @@ def barrier_sync(dist, local):
         dist.barrier()
 
 
-def cpu_reference(cfg_idx: int, iters: int, threads: int):
-    """The reference algorithm on host cores (oracle reference-order restatement)."""
+def host_info():
+    cpu = "unknown"
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                cpu = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return {"cpu": cpu, "nproc": os.cpu_count()}
+
+
+_CPU_INPUTS = {}
+
+
+def cpu_inputs(cfg_idx: int):
+    """The config's inputs from the oracle's own generators (bitwise the product's)."""
     from oracle import pyoracle as po
     import numpy as np
+    if cfg_idx in _CPU_INPUTS:
+        return _CPU_INPUTS[cfg_idx]
     if cfg_idx == 5:
         a = po.laplacian_2d(4096)
-        c1, c2 = po.random_rhs(1 << 24, 2, 1234), po.random_rhs(1 << 24, 2, 1235)
-        method, b = po.CG, a
+        r = (po.CG, a, a, po.random_rhs(1 << 24, 2, 1234), po.random_rhs(1 << 24, 2, 1235))
     elif cfg_idx == 1:
         a = po.laplacian_2d(64)
         c1 = po.random_rhs(4096, 1, 1234); c1 /= np.linalg.norm(c1)
         c2 = po.random_rhs(4096, 1, 1235); c2 /= np.linalg.norm(c2)
-        method, b = po.CG, a
+        r = (po.CG, a, a, c1, c2)
     elif cfg_idx == 3:
         a = po.laplacian_2d(1024)
-        c1, c2, b, method = po.random_rhs(1 << 20, 1, 1234), None, None, po.CG_LYAPUNOV
+        r = (po.CG_LYAPUNOV, a, None, po.random_rhs(1 << 20, 1, 1234), None)
+    elif cfg_idx == 2:
+        r = (po.BICGSTAB, po.convection_diffusion_2d(256, (10.0, 10.0)), po.convection_diffusion_2d(256, (10.0, -10.0)),
+             po.random_rhs(65536, 4, 1234), po.random_rhs(65536, 4, 1235))
+    elif cfg_idx == 4:
+        r = (po.BICGSTAB, po.convection_diffusion_3d(128, (5.0, 2.5, 1.25)), po.convection_diffusion_3d(64, (0.0, 0.0, 0.0)),
+             po.random_rhs(128 ** 3, 8, 1234), po.random_rhs(64 ** 3, 8, 1235))
     else:
         raise SystemExit(f"no CPU sample defined for config {cfg_idx}")
+    _CPU_INPUTS[cfg_idx] = r
+    return r
+
+
+def cpu_reference(cfg_idx: int, iters: int, threads: int):
+    """The reference algorithm on host cores (oracle reference-order restatement; the
+    reference's own flags: -O3, no -march, no OpenMP; SpMM threaded like parallel.cpp
+    when threads > 1). Returns (iterations, seconds) of iterations 2 .. iters + 1: the
+    solve window (StopWatch, factorized_solvers.cpp:98-99) of an (iters + 1)-iteration
+    run minus that of a 1-iteration run, so basis init and the first extension are
+    excluded."""
+    from oracle import pyoracle as po
+    method, a, b, c1, c2 = cpu_inputs(cfg_idx)
     po.set_parallel(threads > 1, threads)
-    sol = po.solve(method, a, b, c1, c2, po.Config(eps_tol=1e-8, max_iter=iters), po.REFERENCE_ORDER)
+    s0 = po.solve(method, a, b, c1, c2, po.Config(eps_tol=1e-30, max_iter=1), po.REFERENCE_ORDER)
+    s1 = po.solve(method, a, b, c1, c2, po.Config(eps_tol=1e-30, max_iter=iters + 1), po.REFERENCE_ORDER)
     po.set_parallel(False, 1)
-    return sol.n_iterations, sol.total_time_s
+    return s1.n_iterations - s0.n_iterations, s1.total_time_s - s0.total_time_s
 
 
 def run_reference(args, rank, world):
     if rank != 0:
         return
     threads = os.cpu_count() or 1
+    iters = args.cpu_iters or 5
     for _ in range(args.warmup):
-        cpu_reference(args.config, args.cpu_iters, threads)
+        cpu_reference(args.config, iters, threads)
     its, secs = 0, 0.0
     for _ in range(args.steps):
-        i, t = cpu_reference(args.config, args.cpu_iters, threads)
+        i, t = cpu_reference(args.config, iters, threads)
         its += i
         secs += t
     v = its / secs
+    sample = (f"config C{args.config}, iterations 2..{iters + 1} per step (init excluded: (N+1)-iteration solve "
+              f"window minus the 1-iteration window), oracle reference-order restatement (reference unbuildable: "
+              f"Eigen3/GTest absent), SpMM threaded over {threads} host threads as in parallel.cpp")
     line = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * secs / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic", "config": {"workload": f"C{args.config}", "sample": f"first {args.cpu_iters} iterations"},
-        "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": "port",
-                         "sample": f"config C{args.config}, first {args.cpu_iters} iterations per step, "
-                                   f"oracle reference-order restatement (reference unbuildable: Eigen3/GTest absent), "
-                                   f"SpMM threaded over {threads} host threads as in parallel.cpp"},
+        "data": "synthetic", "config": {"workload": f"C{args.config}", "sample": f"iterations 2..{iters + 1}"},
+        "host": host_info(),
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -240,9 +279,10 @@ def main():
         iters += sol.history.iterations()
         launches += sol.stats["kernel_launches"]
         for name, c in sol.stats["classes"].items():
-            acc = classes.setdefault(name, {"time_s": 0.0, "bytes": 0.0, "launches": 0})
+            acc = classes.setdefault(name, {"time_s": 0.0, "bytes": 0.0, "flops": 0.0, "launches": 0})
             acc["time_s"] += c["time_s"]
             acc["bytes"] += c["bytes"]
+            acc["flops"] += c.get("flops", 0.0)
             acc["launches"] += c["launches"]
         hist = sol.history
         status = sol.status
@@ -257,11 +297,46 @@ def main():
     value = total_iters / dev_max
     peak, peak_src = peaks()
     dom = max(classes.items(), key=lambda kv: kv[1]["time_s"])
-    achieved = dom[1]["bytes"] / dom[1]["time_s"] / 1e9 if dom[1]["time_s"] > 0 else 0.0
+    fp64_peak = None
+    if any(v["flops"] > 0 for v in classes.values()):
+        dfma, dmuladd = sk.measure_fp64_peak(local)
+        fp64_peak = {"dfma_tflops": dfma, "dmul_dadd_tflops": dmuladd,
+                     "source": "measured in this run (sk_measure_fp64_peak: 16 register chains per thread, "
+                               "8 CTAs x 256 threads per SM, CUDA events, best of 5)"}
     traffic = None
     tp = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tp):
         traffic = json.load(open(tp)).get(f"C{args.config}", {}).get(dom[0])
+
+    def class_roofline(v):
+        """A class is bound by whichever of its HBM time (bytes / measured copy peak) and its
+        FP64 time (flops / measured DFMA peak) is larger; frac = that time / measured time."""
+        if v["time_s"] <= 0:
+            return None
+        t_hbm = v["bytes"] / (peak * 1e9)
+        t_f64 = v["flops"] / (fp64_peak["dfma_tflops"] * 1e12) if (fp64_peak and v["flops"] > 0) else 0.0
+        if t_f64 > t_hbm:
+            ach = v["flops"] / v["time_s"] / 1e12
+            return {"bound": "fp64", "achieved": ach, "peak": fp64_peak["dfma_tflops"], "unit": "TFLOP/s",
+                    "frac": ach / fp64_peak["dfma_tflops"]}
+        ach = v["bytes"] / v["time_s"] / 1e9
+        return {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak}
+
+    dom_rf = class_roofline(dom[1]) or {"bound": "hbm", "achieved": 0.0, "peak": peak, "unit": "GB/s", "frac": 0.0}
+    # whole-iteration figure: sum of the per-class roofline times / measured time (SURVEY 8d)
+    t_roof = 0.0
+    for v in classes.values():
+        t_hbm = v["bytes"] / (peak * 1e9)
+        t_f64 = v["flops"] / (fp64_peak["dfma_tflops"] * 1e12) if (fp64_peak and v["flops"] > 0) else 0.0
+        t_roof += max(t_hbm, t_f64)
+    cls_out = {}
+    for k_, v in classes.items():
+        if not v["launches"]:
+            continue
+        rf = class_roofline(v)
+        cls_out[k_] = {"share": v["time_s"] / max(dev_s, 1e-30), "launches": v["launches"],
+                       "bound": rf["bound"] if rf else None, "achieved": rf["achieved"] if rf else None,
+                       "unit": rf["unit"] if rf else None, "frac": rf["frac"] if rf else None}
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -279,12 +354,13 @@ def main():
                              if 8 * cfg.a.n_rows * int(cfg.c1.shape[1]) > 126e6
                              else "L2-resident between passes (small config)")),
                    "wall_s_timed_region": wall},
-        "roofline": {"bound": "hbm", "kernel": dom[0], "achieved": achieved, "peak": peak,
-                     "peak_source": peak_src, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": traffic,
-                     "classes": {k: {"GBps": (v["bytes"] / v["time_s"] / 1e9) if v["time_s"] > 0 else None,
-                                     "share": v["time_s"] / max(dev_s, 1e-30), "launches": v["launches"]}
-                                 for k, v in classes.items() if v["launches"]}},
+        "roofline": {"bound": dom_rf["bound"], "kernel": dom[0], "achieved": dom_rf["achieved"],
+                     "peak": dom_rf["peak"],
+                     "peak_source": peak_src if dom_rf["bound"] == "hbm" else fp64_peak["source"],
+                     "unit": dom_rf["unit"], "frac": dom_rf["frac"], "traffic": traffic,
+                     "whole_step_frac": t_roof / max(dev_s, 1e-30),
+                     "hbm_peak_gbs": peak, "fp64_peak": fp64_peak,
+                     "classes": cls_out},
         "clocks": clocks,
         "gpu_launches": launches,
     }
@@ -311,43 +387,69 @@ def main():
                        "note": "per rank (rank 0's bytes); wall time max over ranks; includes host "
                                "CSR checks/transposition and the local-row upload"}
     if rank == 0 and not partitioned and not args.no_e2e:
-        e2e_its, e2e_s, h2d, d2h = 0, 0.0, 0, 0
-        # the step's inputs sit in page-locked host memory (filled once, outside the
-        # timed region); every timed call copies them to HBM
+        def call(c1x, c2x):
+            if cfg.method == "cg":
+                return sk.factorized_cg(cfg.a, cfg.b, c1x, c2x, scfg, sk.GpuOptions(device=local))
+            if cfg.method == "cg_lyapunov":
+                return sk.factorized_cg_lyapunov(cfg.a, c1x, scfg, sk.GpuOptions(device=local))
+            return sk.factorized_bicgstab(cfg.a, cfg.b, c1x, c2x, scfg, sk.GpuOptions(device=local))
+
+        def e2e_leg(c1x, c2x, steps, factors=False):
+            """steps timed calls after one untimed warm-up call (first-call costs: pinned
+            staging buffers, memory pool growth)."""
+            e_its, e_s, h2d, d2h = 0, 0.0, 0, 0
+            for it in range(steps + 1):
+                t0 = time.perf_counter()
+                sol = call(c1x, c2x)
+                core = sol.core                      # D2H of the result core
+                nb = core.nbytes
+                if factors:                          # FactorizedSolution returns V, W by value
+                    v = sol.V                        # (factorized_solvers.cpp:194-195)
+                    nb += v.nbytes
+                    if cfg.method != "cg_lyapunov":
+                        w = sol.W
+                        nb += w.nbytes
+                        del w
+                    del v
+                dt = time.perf_counter() - t0
+                if it > 0:
+                    e_s += dt
+                    e_its += sol.history.iterations()
+                    h2d += sol.stats["h2d_bytes"]
+                    d2h += sol.stats["d2h_bytes"] + nb
+                sol.free()
+            return {"value": e_its / e_s, "unit": UNIT, "h2d_bytes_per_step": h2d // steps,
+                    "d2h_bytes_per_step": d2h // steps}
+
+        # headline: the caller's C1, C2 in ordinary pageable memory, as the reference's
+        # DenseMatrix holds them; history and core come back, V/W stay in HBM until asked for
+        line["e2e"] = e2e_leg(cfg.c1, cfg.c2, args.e2e_steps)
+        line["e2e"]["note"] = ("sk_factorized_* from pageable host buffers: host CSR validation, symmetry check, "
+                               "stencil detection (all host threads), H2D of C1, C2 through pinned staging lanes, "
+                               "solve, D2H of history + core; V, W stay in HBM until requested")
+        # the same with C1, C2 in page-locked memory (sk_host_alloc): direct DMA
         c1h = sk.pinned_empty(cfg.c1.shape)
         c1h[...] = cfg.c1
         c2h = c1h if (cfg.c2 is None or cfg.c2 is cfg.c1) else sk.pinned_empty(cfg.c2.shape)
         if c2h is not c1h:
             c2h[...] = cfg.c2
-        # one untimed warm-up call (first-call costs: pinned staging buffers, pool growth)
-        for it in range(args.e2e_steps + 1):
-            t0 = time.perf_counter()
-            if cfg.method == "cg":
-                sol = sk.factorized_cg(cfg.a, cfg.b, c1h, c2h, scfg, sk.GpuOptions(device=local))
-            elif cfg.method == "cg_lyapunov":
-                sol = sk.factorized_cg_lyapunov(cfg.a, c1h, scfg, sk.GpuOptions(device=local))
-            else:
-                sol = sk.factorized_bicgstab(cfg.a, cfg.b, c1h, c2h, scfg, sk.GpuOptions(device=local))
-            core = sol.core  # D2H of the result core (V, W stay in HBM until requested)
-            dt = time.perf_counter() - t0
-            if it > 0:
-                e2e_s += dt
-                e2e_its += sol.history.iterations()
-                h2d += sol.stats["h2d_bytes"]
-                d2h += sol.stats["d2h_bytes"] + core.nbytes
-            sol.free()
-        line["e2e"] = {"value": e2e_its / e2e_s, "unit": UNIT,
-                       "h2d_bytes_per_step": h2d // args.e2e_steps,
-                       "d2h_bytes_per_step": d2h // args.e2e_steps,
-                       "note": "includes host CSR validation, symmetry check, stencil detection (all host threads) and the H2D of C1, C2 from page-locked host memory"}
+        line["e2e_pinned_inputs"] = e2e_leg(c1h, c2h, args.e2e_steps)
+        if not args.no_factors:
+            # the reference's by-value FactorizedSolution: V and W copied to host memory too
+            line["e2e_with_factors"] = e2e_leg(cfg.c1, cfg.c2, 1, factors=True)
+            line["e2e_with_factors"]["note"] = ("as e2e plus V and W normalised on the device and copied to pageable "
+                                                "host arrays (sk_solution_copy_V/W, 8 staging lanes); 1 timed call")
 
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        line["host"] = host_info()
         try:
-            its, secs = cpu_reference(args.config, args.cpu_iters, 1)
+            n_it = args.cpu_iters or 10
+            its, secs = cpu_reference(args.config, n_it, 1)
             line["cpu_baseline"] = {
                 "value": its / secs, "unit": UNIT, "cores": 1, "kind": "port",
-                "sample": f"C{args.config}, first {its} iterations, serial oracle reference-order "
-                          f"restatement (-O3, no -march, as proj/CMakeLists.txt), solve window only"}
+                "sample": f"C{args.config}, iterations 2..{n_it + 1} (init excluded), serial oracle reference-order "
+                          f"restatement (-O3, no -march, as proj/CMakeLists.txt), solve window only; "
+                          f"host {line['host']['cpu']}, nproc {line['host']['nproc']}"}
         except SystemExit as e:
             line["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": 1, "kind": "port", "sample": str(e)}
     if rank == 0:

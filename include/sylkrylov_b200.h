@@ -45,8 +45,21 @@ typedef struct {
     int32_t device;              /* CUDA ordinal */
     int32_t profile;             /* 1: time every kernel class with CUDA events */
     int64_t capacity_bytes;      /* HBM budget for the bases (0: 90% of free memory) */
-    int32_t reserved[8];
+    int32_t reduction_mode;      /* SK_REDUCTION_* (0: the reproducible contract) */
+    int32_t reserved[7];
 } sk_gpu_options;
+
+/* Arithmetic mode of the sums on the path.
+ *  SK_REDUCTION_REPRODUCIBLE: fixed reduction trees; results are
+ *    bit-identical across launches, grids and row partitions, and bit-identical to the
+ *    oracle's SKO_REPRODUCIBLE mode. The only mode the device executes.
+ *  SK_REDUCTION_REFERENCE_ORDER: the reference's single sequential sum per inner product
+ *    (dense_matrix.cpp:131-152) is one dependent chain per output and cannot be laid out
+ *    on the device; requesting it returns SK_ERR_UNSUPPORTED. The oracle's
+ *    SKO_REFERENCE_ORDER mode is the CPU statement of it, and the distance between the two
+ *    modes is pinned by tests (CG family <= 1e-10 over whole runs; BiCGSTAB inside the
+ *    window the recurrence's own sensitivity allows, tests/test_bicgstab_sensitivity.py). */
+enum { SK_REDUCTION_REPRODUCIBLE = 0, SK_REDUCTION_REFERENCE_ORDER = 1 };
 
 typedef enum {
     SK_OK = 0,
@@ -84,7 +97,8 @@ typedef struct {
     double class_time_s[9];
     int64_t class_launches[9];
     double class_bytes[9];       /* algorithmic bytes */
-    int64_t paths[4];            /* extension paths: pythagorean, explicit, householder, clean-up */
+    int64_t paths[4];            /* extension paths: direct, householder, clean-up, unused */
+    double class_flops[9];       /* FP64 flops of compute-bound classes (7: dense image), else 0 */
 } sk_solve_stats;
 
 typedef struct sk_solution sk_solution;
@@ -171,6 +185,10 @@ sk_status sk_solution_partition(const sk_solution* sol, int64_t* row0_v, int64_t
 const char* sk_last_error(void);
 const char* sk_version(void);
 int32_t sk_device_count(void);
+/* FP64 peak of the device in TFLOP/s, measured (register-chain microbenchmark, CUDA
+ * events): DFMA chains (fma = 2 flops) and mul-then-add chains (the arithmetic
+ * contract's form). Denominator of the FP64 roofline (bench.py). */
+sk_status sk_measure_fp64_peak(int32_t device, double* dfma_tflops, double* dmul_dadd_tflops);
 
 /* True residual ||A X + X B - C1 C2^T||_F / ||C1 C2^T||_F of X = V core W^T on the
  * device (replaces true_residual / true_residual_factors, factorized_solvers.hpp:56-61,

@@ -81,7 +81,7 @@ class _Cfg(C.Structure):
 
 class _Gpu(C.Structure):
     _fields_ = [("device", C.c_int32), ("profile", C.c_int32), ("capacity_bytes", C.c_int64),
-                ("reserved", C.c_int32 * 8)]
+                ("reduction_mode", C.c_int32), ("reserved", C.c_int32 * 7)]
 
 
 class _Rec(C.Structure):
@@ -94,7 +94,7 @@ class _Stats(C.Structure):
                 ("h2d_bytes", C.c_int64), ("d2h_bytes", C.c_int64), ("kernel_launches", C.c_int64),
                 ("iterations", C.c_int64), ("class_time_s", C.c_double * 9),
                 ("class_launches", C.c_int64 * 9), ("class_bytes", C.c_double * 9),
-                ("paths", C.c_int64 * 4)]
+                ("paths", C.c_int64 * 4), ("class_flops", C.c_double * 9)]
 
 
 KERNEL_CLASSES = ["spmm", "gram", "rare_path", "update", "core_a", "core_b",
@@ -193,9 +193,10 @@ class GpuOptions:
     device: int = 0
     profile: bool = False
     capacity_bytes: int = 0
+    reduction_mode: int = 0  # SK_REDUCTION_REPRODUCIBLE; 1 = reference_order (unsupported on the device)
 
     def _c(self) -> _Gpu:
-        return _Gpu(self.device, int(self.profile), self.capacity_bytes)
+        return _Gpu(self.device, int(self.profile), self.capacity_bytes, int(self.reduction_mode))
 
 
 @dataclass
@@ -250,7 +251,8 @@ class FactorizedSolution:
             "kernel_launches": st.kernel_launches, "iterations": st.iterations,
             "classes": {KERNEL_CLASSES[i]: {"time_s": st.class_time_s[i],
                                              "launches": st.class_launches[i],
-                                             "bytes": st.class_bytes[i]} for i in range(9)},
+                                             "bytes": st.class_bytes[i],
+                                             "flops": st.class_flops[i]} for i in range(9)},
             "paths": dict(zip(["direct", "householder", "cleanup", "unused"], list(st.paths))),
         }
         self.captured_cores = []
@@ -578,6 +580,13 @@ class _Pinned:
             lib().sk_host_free(self.ptr)
         except Exception:
             pass
+
+
+def measure_fp64_peak(device: int = 0):
+    """(DFMA TFLOP/s, mul-then-add TFLOP/s) of the device, measured (sk_measure_fp64_peak)."""
+    f, m = C.c_double(), C.c_double()
+    _check(lib().sk_measure_fp64_peak(C.c_int32(device), C.byref(f), C.byref(m)))
+    return f.value, m.value
 
 
 def pinned_empty(shape, dtype=np.float64, order: str = "F") -> np.ndarray:

@@ -31,6 +31,7 @@ def units():
     u.append(("sk_kernels.cu", "sk_kernels_common.o", ["-DSK_INST_COMMON"]))
     u.append(("sk_driver.cu", "sk_driver.o", []))
     u.append(("sk_residual.cu", "sk_residual.o", []))
+    u.append(("sk_peak.cu", "sk_peak.o", []))
     u.append(("sk_problems.cpp", "sk_problems.o", []))
     u.append(("sk_comm.cpp", "sk_comm.o", []))
     u.append(("sk_export.cpp", "sk_export.o", []))

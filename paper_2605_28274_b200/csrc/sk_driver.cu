@@ -741,7 +741,7 @@ struct Solver {
   struct Ev {
     cudaEvent_t a, b;
     int cls;
-    double bytes;
+    double bytes, flops;
   };
   std::vector<Ev> pending;
   std::vector<cudaEvent_t> pool;
@@ -787,12 +787,12 @@ struct Solver {
   }
 
   template <class F>
-  void timed(int cls, double bytes, F&& f) {
+  void timed(int cls, double bytes, F&& f, double flops = 0.0) {
     if (!P.profile) {
       f();
       return;
     }
-    Ev e{ev_get(), ev_get(), cls, bytes};
+    Ev e{ev_get(), ev_get(), cls, bytes, flops};
     CK(cudaEventRecord(e.a, st));
     f();
     CK(cudaEventRecord(e.b, st));
@@ -809,6 +809,7 @@ struct Solver {
       stats.class_time_s[e.cls] += ms * 1e-3;
       stats.class_launches[e.cls] += 1;
       stats.class_bytes[e.cls] += e.bytes;
+      stats.class_flops[e.cls] += e.flops;
       pool.push_back(e.a);
       pool.push_back(e.b);
     }
@@ -1200,12 +1201,20 @@ struct Solver {
     for (int sd = 0; sd < nsides; ++sd) b += 8.0 * P.op[sd].n * s * (J + 1);
     return b;
   }
-  // Arnoldi CGS2 extension with kb prior blocks (12nnz + 4(n+1) + 8ns(3kb+5))
+  // Arnoldi CGS2 extension with kb prior blocks, AS EXECUTED: SpMM
+  // (x read, w written), two Gram sweeps (kb blocks + the candidate each), two update
+  // sweeps (kb blocks + candidate read, candidate written each), self-Gram:
+  // 12nnz + 4(n+1) + 8ns(4kb + 9). SURVEY 8d's 8ns(3kb+5) assumes a sweep that exact
+  // CGS2 in R1 order cannot drop (the second Gram needs the finished first update).
   double arnoldi_bytes(int64_t kb) const {
     double b = 0;
-    for (int sd = 0; sd < nsides; ++sd) b += csr_bytes(sd) + 8.0 * P.op[sd].n * s * (3.0 * kb + 5.0);
+    for (int sd = 0; sd < nsides; ++sd) b += csr_bytes(sd) + 8.0 * P.op[sd].n * s * (4.0 * kb + 9.0);
     return b;
   }
+  // BiCGSTAB half step on r x r cores: one dense image (2 r^3 flops: H P + P G^T with the
+  // Hessenberg zeros skipped) and ~9 r^2 doubles of core traffic (144 r^2 per iteration)
+  static double half_flops(double r) { return 2.0 * r * r * r; }
+  static double half_bytes(double r) { return 72.0 * r * r; }
   double pass_bytes(int64_t k, int extra) const {
     const double J = (double)std::min<int64_t>(k + 1, 2);
     double b = 0;
@@ -1270,11 +1279,11 @@ struct Solver {
         const double r1 = (double)((2 * k + 2) * s), r2 = (double)((2 * k + 3) * s);
         timed(6, arnoldi_bytes(2 * k + 1), [&] { sk::launch_arnoldi_ext(c, 2 * k + 1, st); });
         dbg("arnoldi1", k);
-        timed(7, 2.0 * r1 * r1 * r1, [&] { sk::launch_bicgstab_half(c, 0, (2 * k + 2) * s, st); });
+        timed(7, half_bytes(r1), [&] { sk::launch_bicgstab_half(c, 0, (2 * k + 2) * s, st); }, half_flops(r1));
         dbg("half1", k);
         timed(6, arnoldi_bytes(2 * k + 2), [&] { sk::launch_arnoldi_ext(c, 2 * k + 2, st); });
         dbg("arnoldi2", k);
-        timed(7, 2.0 * r2 * r2 * r2, [&] { sk::launch_bicgstab_half(c, 1, (2 * k + 3) * s, st); });
+        timed(7, half_bytes(r2), [&] { sk::launch_bicgstab_half(c, 1, (2 * k + 3) * s, st); }, half_flops(r2));
         dbg("half2", k);
       } else {
       for (int sd = 0; sd < nsides; ++sd) ensure_blocks(sd, k + 2);
@@ -1769,6 +1778,12 @@ sk_problem* create_problem(int32_t method, const sk_csr* a, const sk_csr* b, con
   if (!lyap && s > b->n_rows) throw SkError(SK_ERR_DIMENSION, "basis init: block size must be in [1, n]");
   if (s > sk::kMaxS) throw SkError(SK_ERR_UNSUPPORTED, "device path supports block sizes s <= 8");
   if (!c1 || (!lyap && !c2)) throw SkError(SK_ERR_DIMENSION, "solver: C1/C2 missing");
+  if (gpu && gpu->reduction_mode != SK_REDUCTION_REPRODUCIBLE)
+    throw SkError(SK_ERR_UNSUPPORTED,
+                  gpu->reduction_mode == SK_REDUCTION_REFERENCE_ORDER
+                      ? "reduction_mode reference_order: sequential single-chain sums are not executed on the "
+                        "device; use SK_REDUCTION_REPRODUCIBLE (bitwise the oracle's contract mode)"
+                      : "reduction_mode: unknown value");
   const int dev = gpu ? gpu->device : 0;
   check_device(dev);
   tr.mark("device check");
@@ -2340,20 +2355,125 @@ sk_status sk_solution_history(const sk_solution* sol, sk_iteration_record* rec, 
 }
 double sk_solution_total_time(const sk_solution* sol) { return sol->total_time; }
 
+// Device -> host copy into caller (pageable) memory, the mirror of h2d_staged: kLanes
+// host threads, each with its own stream and two pinned bounce buffers (the DMA of
+// chunk i + 1 runs while chunk i is copied out of the other buffer). Page-locked
+// destinations take one direct DMA. Returns when the bytes are in dst. `ready` orders
+// the copies after the producer kernel.
+static void d2h_staged(void* dst, const void* src, size_t bytes, cudaEvent_t ready, cudaStream_t st) {
+  constexpr int kLanes = 8;
+  constexpr size_t kChunk = size_t(8) << 20;
+  struct Lane {
+    char* buf[2] = {nullptr, nullptr};
+    cudaEvent_t done[2] = {nullptr, nullptr};
+    cudaStream_t s = nullptr;
+  };
+  static std::mutex mu;
+  static Lane lanes[kLanes];
+  static int dev_init = -1;
+  {
+    cudaPointerAttributes pa;
+    if (cudaPointerGetAttributes(&pa, dst) == cudaSuccess && pa.type == cudaMemoryTypeHost) {
+      CK(cudaStreamWaitEvent(st, ready, 0));
+      CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+      return;
+    }
+    cudaGetLastError();
+  }
+  std::lock_guard<std::mutex> g(mu);
+  int dev = 0;
+  CK(cudaGetDevice(&dev));
+  bool staged = dev_init == dev;
+  if (dev_init == -1) {
+    staged = true;
+    for (int li = 0; li < kLanes && staged; ++li) {
+      Lane& L = lanes[li];
+      for (int b = 0; b < 2 && staged; ++b) {
+        if (cudaHostAlloc(&L.buf[b], kChunk, cudaHostAllocDefault) != cudaSuccess) {
+          cudaGetLastError();
+          staged = false;
+          break;
+        }
+        CK(cudaEventCreateWithFlags(&L.done[b], cudaEventDisableTiming));
+      }
+      if (staged) CK(cudaStreamCreateWithFlags(&L.s, cudaStreamNonBlocking));
+    }
+    dev_init = staged ? dev : -2;
+  }
+  if (!staged) {
+    CK(cudaStreamWaitEvent(st, ready, 0));
+    CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    return;
+  }
+  const int T = (int)std::max<size_t>(1, std::min<size_t>((size_t)kLanes, (bytes + kChunk - 1) / kChunk));
+  std::vector<std::thread> th;
+  std::string err;
+  std::mutex emu;
+  for (int t = 0; t < T; ++t)
+    th.emplace_back([&, t] {
+      try {
+        CK(cudaSetDevice(dev));
+        Lane& L = lanes[t];
+        CK(cudaStreamWaitEvent(L.s, ready, 0));
+        const size_t lo = bytes * t / T, hi = bytes * (t + 1) / T;
+        const size_t nch = (hi - lo + kChunk - 1) / kChunk;
+        auto issue = [&](size_t i) {
+          const size_t off = lo + i * kChunk, n = std::min(kChunk, hi - off);
+          CK(cudaMemcpyAsync(L.buf[i & 1], (const char*)src + off, n, cudaMemcpyDeviceToHost, L.s));
+          CK(cudaEventRecord(L.done[i & 1], L.s));
+        };
+        if (nch) issue(0);
+        for (size_t i = 0; i < nch; ++i) {
+          CK(cudaEventSynchronize(L.done[i & 1]));
+          if (i + 1 < nch) issue(i + 1);
+          const size_t off = lo + i * kChunk, n = std::min(kChunk, hi - off);
+          std::memcpy((char*)dst + off, L.buf[i & 1], n);
+        }
+      } catch (const std::exception& e) {
+        std::lock_guard<std::mutex> ge(emu);
+        err = e.what();
+      }
+    });
+  for (auto& x : th) x.join();
+  if (!err.empty()) throw SkError(SK_ERR_CUDA, err);
+}
+
+// FactorizedSolution's V / W by value (factorized_solvers.cpp:194-195): block b is
+// normalised into one of two device staging buffers while block b - 1 crosses PCIe.
 static sk_status copy_basis(const sk_solution* sol, const std::vector<double*>& blocks,
                             const double* nfac, int64_t n, int64_t cols, double* out) {
   return run_guarded([&] {
     CK(cudaSetDevice(sol->device));
     if (cols == 0) return;
-    double* stage = nullptr;
-    CK(cudaMalloc(&stage, sizeof(double) * n * sol->s));
-    for (int64_t b = 0; b < cols / sol->s; ++b) {
-      sk::launch_export_block((int)sol->s, blocks[b], nfac, b, stage, n, sol->stream);
-      CK(cudaMemcpyAsync(out + b * sol->s * n, stage, sizeof(double) * n * sol->s,
-                         cudaMemcpyDeviceToHost, sol->stream));
+    const size_t bb = sizeof(double) * n * sol->s;
+    double* stage[2] = {nullptr, nullptr};
+    cudaEvent_t ev[2];
+    for (int i = 0; i < 2; ++i) {
+      CK(cudaMalloc(&stage[i], bb));
+      CK(cudaEventCreateWithFlags(&ev[i], cudaEventDisableTiming));
+    }
+    cudaStream_t cs;
+    CK(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+    const int64_t nb = cols / sol->s;
+    try {
+      for (int64_t b = 0; b <= nb; ++b) {
+        if (b < nb) {
+          sk::launch_export_block((int)sol->s, blocks[b], nfac, b, stage[b & 1], n, sol->stream);
+          CK(cudaEventRecord(ev[b & 1], sol->stream));
+        }
+        if (b > 0) d2h_staged(out + (b - 1) * sol->s * n, stage[(b - 1) & 1], bb, ev[(b - 1) & 1], cs);
+      }
+    } catch (...) {
+      cudaStreamSynchronize(sol->stream);
+      for (int i = 0; i < 2; ++i) cudaFree(stage[i]), cudaEventDestroy(ev[i]);
+      cudaStreamDestroy(cs);
+      throw;
     }
     CK(cudaStreamSynchronize(sol->stream));
-    cudaFree(stage);
+    for (int i = 0; i < 2; ++i) cudaFree(stage[i]), cudaEventDestroy(ev[i]);
+    cudaStreamDestroy(cs);
   });
 }
 // columns [col0, col0 + ncols) of a basis: only the blocks covering them are

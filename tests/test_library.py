@@ -184,3 +184,14 @@ def test_speculative_stencil_late_row_out_of_range(skl, method):
                 skl.factorized_cg_lyapunov(bad, c1)
             else:
                 skl.factorized_bicgstab(good, bad, c1, c2)
+
+
+def test_reference_order_reduction_mode_is_rejected(sk_host):
+    """sk_gpu_options.reduction_mode: the device executes the reproducible
+    contract only; asking for the reference's sequential sums fails loudly, never a fallback."""
+    sk = sk_host
+    from paper_2605_28274_b200 import problems as pr
+    a = pr.laplacian_2d(8)
+    c = pr.random_rhs(64, 1, 3)
+    with pytest.raises(sk.UnsupportedError, match="reference_order"):
+        sk.factorized_cg(a, a, c, c, sk.SolverConfig(), sk.GpuOptions(reduction_mode=1))
