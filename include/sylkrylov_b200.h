@@ -207,6 +207,16 @@ sk_status sk_true_residual_factors(const sk_csr* a, const sk_csr* b, const doubl
                                    const double* w, int64_t rw, double* rel);
 sk_status sk_problem_true_residual(const sk_problem* p, const sk_solution* sol, double* rel);
 
+/* X-parity through factor products (the stacked-factor pattern of
+ * true_residual_factors, factorized_solvers.cpp:410-438): r_out (column-major,
+ * (r + ref_cols)^2, upper triangular) = the R factor of [V_sol, V_ref] (side 0) or
+ * [W_sol, W_ref] (side 1), V_sol read where the solution holds it (HBM), V_ref a host
+ * column-major rows x ref_cols matrix (e.g. the CPU oracle's factors). Then
+ * ||X_sol - X_ref||_F = ||R_V diag(core_sol, -core_ref) R_W^T||_F. Streaming TSQR on the
+ * device; floating point outside the bitwise contract. */
+sk_status sk_solution_stacked_r(const sk_solution* sol, int32_t side, const double* ref, int64_t ref_cols,
+                                double* r_out);
+
 /* Kernel-level entry for parity tests: y = A x (reference spmm order) or
  * y = A^T x (spmm_transpose, via the transposed CSR) on the device. */
 sk_status sk_spmm(const sk_csr* a, const double* x, int64_t s, int32_t transpose, double* y);

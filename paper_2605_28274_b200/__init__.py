@@ -450,6 +450,35 @@ def true_residual_factors(a: SparseMatrix, b: SparseMatrix, c1, c2, v, core, w) 
     return out.value
 
 
+def x_distance(sol: FactorizedSolution, v_ref, core_ref, w_ref, lyapunov: bool = False):
+    """||X_sol - X_ref||_F / ||X_ref||_F with X = V core W^T on both sides, through factor
+    products only (the stacked-factor QR of factorized_solvers.cpp:410-438):
+    R_V = qr([V_sol, V_ref]).R and R_W = qr([W_sol, W_ref]).R by the device's streaming TSQR
+    (sk_solution_stacked_r: V_sol, W_sol never leave HBM), then the small product
+    R_V diag(core_sol, -core_ref) R_W^T on the host. Returns (relative distance, ||X_ref||_F)."""
+    v_ref = np.asfortranarray(np.asarray(v_ref, dtype=np.float64))
+    w_ref = v_ref if lyapunov else np.asfortranarray(np.asarray(w_ref, dtype=np.float64))
+    core_ref = np.asarray(core_ref, dtype=np.float64)
+    if v_ref.shape[0] != sol.n or w_ref.shape[0] != sol.m or core_ref.shape != (v_ref.shape[1], w_ref.shape[1]):
+        raise DimensionError("x_distance: reference factor shapes do not conform")
+
+    def stacked(side, ref, r_own):
+        wdt = r_own + ref.shape[1]
+        out = np.zeros((wdt, wdt), order="F")
+        _check(lib().sk_solution_stacked_r(sol._h, C.c_int32(side), _p(ref), C.c_int64(ref.shape[1]), _p(out)))
+        return np.triu(out)
+
+    rv = stacked(0, v_ref, sol.rv)
+    rw = rv if (lyapunov and sol.rw == sol.rv) else stacked(1, w_ref, sol.rw)
+    core = sol.core
+    mid = np.zeros((rv.shape[0], rw.shape[0]))
+    mid[:sol.rv, :sol.rw] = core
+    mid[sol.rv:, sol.rw:] = -core_ref
+    diff = np.linalg.norm(rv @ mid @ rw.T)
+    ref_norm = np.linalg.norm(rv[:, sol.rv:] @ core_ref @ rw[:, sol.rw:].T)
+    return float(diff / ref_norm), float(ref_norm)
+
+
 def spmm(a: SparseMatrix, x, transpose: bool = False) -> np.ndarray:
     """Device SpMM (K1) in the reference's per-row order (sparse_matrix.cpp:142-200)."""
     x = np.asfortranarray(np.asarray(x, dtype=np.float64))

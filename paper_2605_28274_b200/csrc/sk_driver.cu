@@ -2219,6 +2219,80 @@ sk_status sk_true_residual_factors(const sk_csr* a, const sk_csr* b, const doubl
   });
 }
 
+// X-parity at scale (SURVEY 8c "factor-Gram X-parity metric", 8f-1): the R factor of the
+// stacked basis [V_sol, V_ref] (side 0) or [W_sol, W_ref] (side 1) by the same streaming TSQR
+// as the true residual. V_sol's rows come from the raw blocks in HBM (normalised on the fly);
+// V_ref is the caller's host matrix (column-major rows x ref_cols, e.g. the CPU oracle's
+// reference-order factors), uploaded chunk by chunk straight into the QR workspace. With
+// R_V, R_W the distance is ||R_V diag(core_sol, -core_ref) R_W^T||_F (the pattern of
+// true_residual_factors, factorized_solvers.cpp:410-438), formed by the caller from the
+// small factors: no n x r product, no sqrt(eps) floor of the inner-product expansion.
+sk_status sk_solution_stacked_r(const sk_solution* sol, int32_t side, const double* ref, int64_t ref_cols,
+                                double* r_out) {
+  return run_guarded([&] {
+    if (!sol || !r_out || (ref_cols > 0 && !ref) || ref_cols < 0 || (side != 0 && side != 1))
+      throw SkError(SK_ERR_DIMENSION, "stacked_r: bad arguments");
+    if (sol->row0_v != 0 || sol->row0_w != 0 || (sol->rv > 0 && sol->vblocks.empty()))
+      throw SkError(SK_ERR_UNSUPPORTED, "stacked_r: row-partitioned solutions are not supported");
+    const auto& blocks = side == 0 ? sol->vblocks : sol->wblocks;
+    const double* nfac = side == 0 ? sol->vnfac : sol->wnfac;
+    const int64_t n = side == 0 ? sol->n : sol->m;
+    const int64_t kb64 = side == 0 ? sol->rv : sol->rw;
+    if (kb64 + ref_cols >= 46341 || n >= (int64_t(1) << 31))
+      throw SkError(SK_ERR_UNSUPPORTED, "stacked_r: sizes beyond the device path's int32 limits");
+    const int kb = (int)kb64, wdt = kb + (int)ref_cols, bs = (int)sol->s, nblk = kb / bs;
+    if (wdt == 0) return;
+    CK(cudaSetDevice(sol->device));
+    cudaStream_t st;
+    CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    struct SG {
+      cudaStream_t s;
+      ~SG() { cudaStreamDestroy(s); }
+    } sg{st};
+    TrHandles h(st);
+    size_t fr = 0, tot = 0;
+    CK(cudaMemGetInfo(&fr, &tot));
+    const double budget = std::min<double>((double)fr / 3.0, 8.0e9);
+    int64_t rc = (int64_t)(budget / (8.0 * (kb + 2.0 * wdt)));
+    rc = std::max<int64_t>(rc, 256);
+    if (const char* e = getenv("SK_TR_CHUNK")) rc = std::max<int64_t>(1, std::atoll(e));
+    rc = std::min<int64_t>(rc, n);
+    const int64_t ldm = wdt + rc;
+    DevBuf mem;
+    const double** tb = mem.get<const double*>(std::max(nblk, 1));
+    if (nblk) CK(cudaMemcpyAsync(tb, blocks.data(), sizeof(double*) * nblk, cudaMemcpyHostToDevice, st));
+    double* G = mem.get<double>((size_t)rc * std::max(kb, 1));
+    double* M = mem.get<double>((size_t)ldm * wdt);
+    double* tau = mem.get<double>(wdt);
+    int* info = mem.get<int>(1);
+    int lwork = 0;
+    CKS(cusolverDnDgeqrf_bufferSize(h.cs, (int)ldm, wdt, M, (int)ldm, &lwork));
+    double* work = mem.get<double>((size_t)lwork);
+    CK(cudaMemsetAsync(M, 0, sizeof(double) * ldm * wdt, st));
+    for (int64_t r0 = 0; r0 < n; r0 += rc) {
+      const int64_t rows = std::min<int64_t>(rc, n - r0);
+      if (rows < rc)  // last, shorter chunk: clear the rows the previous chunk left below it
+        for (int j = 0; j < wdt; ++j)
+          CK(cudaMemsetAsync(M + (int64_t)j * ldm + wdt + rows, 0, sizeof(double) * (rc - rows), st));
+      if (nblk) {
+        sk::launch_tr_gather_blocks(tb, nfac, bs, nblk, n, r0, rows, G, st);
+        sk::launch_tr_fill_rows(M, ldm, wdt, rows, G, kb, st);
+      }
+      if (ref_cols)
+        CK(cudaMemcpy2DAsync(M + (int64_t)kb * ldm + wdt, sizeof(double) * ldm, ref + r0, sizeof(double) * n,
+                             sizeof(double) * rows, (size_t)ref_cols, cudaMemcpyHostToDevice, st));
+      CKS(cusolverDnDgeqrf(h.cs, (int)(wdt + rows), wdt, M, (int)ldm, tau, work, lwork, info));
+      sk::launch_tr_keep_r(M, ldm, wdt, st);
+    }
+    CK(cudaMemcpy2DAsync(r_out, sizeof(double) * wdt, M, sizeof(double) * ldm, sizeof(double) * wdt, wdt,
+                         cudaMemcpyDeviceToHost, st));
+    int hinfo = 0;
+    CK(cudaMemcpyAsync(&hinfo, info, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (hinfo != 0) throw SkError(SK_ERR_CUDA, "stacked_r: geqrf reported an illegal argument");
+  });
+}
+
 sk_status sk_problem_true_residual(const sk_problem* p, const sk_solution* sol, double* rel) {
   return run_guarded([&] {
     if (!p || !sol || !rel) throw SkError(SK_ERR_DIMENSION, "true_residual: null argument");

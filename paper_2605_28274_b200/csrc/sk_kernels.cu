@@ -746,6 +746,22 @@ struct GramSplit {
   static constexpr int UNR = H == 2 ? 2 : 4;
   static constexpr int MINB = H == 2 ? 2 : (S <= 4 ? 3 : 1);  // CTAs per SM (register budget)
 };
+#ifndef SK_GRAM_RING
+#define SK_GRAM_RING 1
+#endif
+#ifndef SK_GRAM_STAGES
+#define SK_GRAM_STAGES 3
+#endif
+constexpr int kGramStages = SK_GRAM_STAGES;
+// shared-memory row ring of k_gram (even S: 16-byte aligned rows): per lane S doubles of
+// U_b and S / H of x, padded to an odd number of 16-byte units
+template <int S>
+struct GramRing {
+  static constexpr bool ON = (S % 2 == 0);
+  static constexpr int UNITS = (S + S / GramSplit<S>::H) / 2;
+  static constexpr int STRIDE = 2 * (UNITS | 1);  // doubles
+  static constexpr size_t BYTES = ON ? sizeof(double) * (size_t)8 * kGramStages * 32 * STRIDE : 0;
+};
 template <int S>
 __global__ void __launch_bounds__(256, GramSplit<S>::MINB) k_gram(const __grid_constant__ SolveConst c, int mode) {
   constexpr int NB = S * S;
@@ -773,6 +789,79 @@ __global__ void __launch_bounds__(256, GramSplit<S>::MINB) k_gram(const __grid_c
   const SegGeom g = seg_geom(cta, sc.nseg);
   double* part = sc.part + ((by * sc.ncta + cta) * NB) + h * NH;  // entries u*S+t, u in this half
   OwnerVals<NH> segv[kSegsPerWarp];
+#if SK_GRAM_RING
+  if constexpr (GramRing<S>::ON) {
+    // Rows reach the registers through a per-warp shared-memory ring filled by cp.async
+    // kGramStages - 1 row steps ahead (a lane copies its own row of U_b and of x and reads
+    // back only what it copied: no barrier; the lane stride is an odd number of 16-byte
+    // units, so both directions are conflict-free). The loads of step t + D - 1 are in
+    // flight while step t is accumulated; the per-lane order m = 0..15 of R1 is unchanged.
+    constexpr int D = kGramStages, ST = GramRing<S>::STRIDE;
+    extern __shared__ __align__(16) double gram_ring[];
+    double* my = gram_ring + ((size_t)(threadIdx.x >> 5) * D * 32 + lane) * ST;
+    const int nsteps = g.nvalid_warp * kLRows;
+    auto issue = [&](int step) {
+      if (step < nsteps) {
+        const int64_t i = (g.seg_w0 + step / kLRows) * kSeg + lane + 32 * (step % kLRows);
+        if (i < n) {
+          const unsigned d = (unsigned)__cvta_generic_to_shared(my + (size_t)(step % D) * 32 * ST);
+          const double* ga = ub + i * S;
+          const double* gy = x + i * S + h * SU;
+#pragma unroll
+          for (int t = 0; t < S / 2; ++t)
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d + 16 * t), "l"(ga + 2 * t) : "memory");
+#pragma unroll
+          for (int u = 0; u < SU / 2; ++u)
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(d + 8 * S + 16 * u), "l"(gy + 2 * u)
+                         : "memory");
+        }
+      }
+      asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+#pragma unroll
+    for (int p_ = 0; p_ < D - 1; ++p_) issue(p_);
+#pragma unroll
+    for (int q = 0; q < kSegsPerWarp; ++q) {
+      double acc[NH];
+#pragma unroll
+      for (int e = 0; e < NH; ++e) acc[e] = 0.0;
+      if (q < g.nvalid_warp) {
+        const int64_t base = (g.seg_w0 + q) * kSeg;
+#pragma unroll 2
+        for (int m = 0; m < kLRows; ++m) {
+          const int step = q * kLRows + m;
+          issue(step + D - 1);
+          asm volatile("cp.async.wait_group %0;" ::"n"(D - 1) : "memory");
+          const int64_t i = base + lane + 32 * m;
+          if (i < n) {
+            const double* sp = my + (size_t)(step % D) * 32 * ST;
+            double a[S], y[SU];
+#pragma unroll
+            for (int t = 0; t < S / 2; ++t) {
+              const double2 v = reinterpret_cast<const double2*>(sp)[t];
+              a[2 * t] = v.x;
+              a[2 * t + 1] = v.y;
+            }
+#pragma unroll
+            for (int u = 0; u < SU / 2; ++u) {
+              const double2 v = reinterpret_cast<const double2*>(sp + S)[u];
+              y[2 * u] = v.x;
+              y[2 * u + 1] = v.y;
+            }
+#pragma unroll
+            for (int u = 0; u < SU; ++u)
+#pragma unroll
+              for (int t = 0; t < S; ++t)
+                acc[u * S + t] = __dadd_rn(acc[u * S + t], __dmul_rn(a[t], y[u]));
+          }
+        }
+      }
+      seg_butterfly<NH>(acc, segv[q], lane);
+    }
+    asm volatile("cp.async.wait_all;" ::: "memory");
+  } else
+#endif
+  {
 #pragma unroll
   for (int q = 0; q < kSegsPerWarp; ++q) {
     double acc[NH];
@@ -806,6 +895,7 @@ __global__ void __launch_bounds__(256, GramSplit<S>::MINB) k_gram(const __grid_c
       }
     }
     seg_butterfly<NH>(acc, segv[q], lane);
+  }
   }
   cta_combine<NH>(segv, g.nvalid_warp, g.nvalid_cta, part);
 
@@ -1596,11 +1686,24 @@ __global__ void __launch_bounds__(kCsThreads, 1)
 #pragma unroll
     for (int t = 0; t < S; ++t) cup[q][t] = cce[q][t] = kup[q][t] = kce[q][t] = 0.0;
 #endif
+#ifdef SK_CS_PROF2
+  long long pf_wait = 0, pf_work = 0, pf_mb = 0, pf_a = clock64();
+#endif
   // steps for lines y0-1 .. y1 (U_k with one halo line each side) + one drain step
   for (int y = ys; y <= y1 + 1; ++y) {
 #if SK_CS_TMA
+#ifdef SK_CS_PROF2
+    const long long pf_m0 = clock64();
+#endif
     if (issuer && lane == 0) mb_wait(&mbar[(y - ys) & 7], (unsigned)((y - ys) >> 3) & 1u);
+#ifdef SK_CS_PROF2
+    pf_mb += clock64() - pf_m0;
+#endif
     __syncthreads();
+#ifdef SK_CS_PROF2
+    const long long pf_b = clock64();
+    pf_wait += pf_b - pf_a;
+#endif
     // group G(y): U_{k-1} line y + 5, U_{k-2} line y + 4 (consumed at step y + 4;
     // the slots' last readers finished before this step's barrier)
     if (issuer && y + 4 <= y1 + 1) issue(y - ys + 4, y + 5, y + 5, y + 4);
@@ -1781,7 +1884,16 @@ __global__ void __launch_bounds__(kCsThreads, 1)
         }
       }
     }
+#ifdef SK_CS_PROF2
+    pf_a = clock64();
+    pf_work += pf_a - pf_b;
+#endif
   }
+#ifdef SK_CS_PROF2
+  if (lane == 0 && blockIdx.x == 5 && side == 0 && (k == 100 || k == 101))
+    printf("CSW2 k %lld warp %d steps %d wait %lld (mbarrier %lld) work %lld\n", (long long)k, warp, y1 + 2 - ys,
+           pf_wait, pf_mb, pf_work);
+#endif
   asm volatile("cp.async.wait_all;" ::: "memory");
   unsigned* ctr = sc.sctr;  // [0..nranges) per range, [nranges] per side
 #ifdef SK_CS_PROF
@@ -2998,8 +3110,17 @@ struct Launch {
   static void gram(const SolveConst& c, int mode, int64_t nblk, cudaStream_t st) {
     int64_t nmax, cmax;
     dims(c, nmax, cmax);
-    k_gram<S><<<dim3((unsigned)((nblk > 0 ? nblk : 1) * GramSplit<S>::H), (unsigned)cmax, c.nsides), 256, 0, st>>>(
-        c, mode);
+    size_t smem = 0;
+#if SK_GRAM_RING
+    smem = GramRing<S>::BYTES;
+    static bool attr = false;
+    if (smem > 48 * 1024 && !attr) {
+      cudaFuncSetAttribute(k_gram<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      attr = true;
+    }
+#endif
+    k_gram<S><<<dim3((unsigned)((nblk > 0 ? nblk : 1) * GramSplit<S>::H), (unsigned)cmax, c.nsides), 256, smem,
+                st>>>(c, mode);
   }
   static void update(const SolveConst& c, int mode, cudaStream_t st) {
     int64_t nmax, cmax;

@@ -47,4 +47,6 @@ void launch_tr_apply(const TrOp& op, const double* X, int64_t h, int64_t r0, int
 void launch_tr_fill(double* M, int64_t ldm, int64_t off, int64_t rows, const double* C, int64_t n, int s, int64_t r0,
                     const double* P1, int64_t h1, const double* P2, int64_t h2, int r, double sgn, cudaStream_t st);
 void launch_tr_keep_r(double* M, int64_t ldm, int wdt, cudaStream_t st);
+void launch_tr_fill_rows(double* M, int64_t ldm, int64_t off, int64_t rows, const double* G, int cols,
+                         cudaStream_t st);
 }  // namespace sk

@@ -126,6 +126,18 @@ __global__ void k_tr_keep_r(double* __restrict__ M, int64_t ldm, int wdt) {
   }
 }
 
+// M (column-major, ldm) rows [off, off + rows), columns [0, cols) <- G (row-major rows x cols)
+__global__ void k_tr_fill_rows(double* __restrict__ M, int64_t ldm, int64_t off, int64_t rows,
+                               const double* __restrict__ G, int cols) {
+  const int64_t total = rows * cols;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t ii = idx % rows;
+    const int c = (int)(idx / rows);
+    M[(int64_t)c * ldm + off + ii] = G[ii * cols + c];
+  }
+}
+
 static unsigned tr_grid(int64_t total) {
   int64_t g = (total + 255) / 256;
   return (unsigned)(g < 1 ? 1 : (g > 148 * 32 ? 148 * 32 : g));
@@ -145,6 +157,10 @@ void launch_tr_apply(const TrOp& op, const double* X, int64_t h, int64_t r0, int
 void launch_tr_fill(double* M, int64_t ldm, int64_t off, int64_t rows, const double* C, int64_t n, int s, int64_t r0,
                     const double* P1, int64_t h1, const double* P2, int64_t h2, int r, double sgn, cudaStream_t st) {
   k_tr_fill<<<tr_grid(rows * (s + 2 * r)), 256, 0, st>>>(M, ldm, off, rows, C, n, s, r0, P1, h1, P2, h2, r, sgn);
+}
+void launch_tr_fill_rows(double* M, int64_t ldm, int64_t off, int64_t rows, const double* G, int cols,
+                         cudaStream_t st) {
+  k_tr_fill_rows<<<tr_grid(rows * cols), 256, 0, st>>>(M, ldm, off, rows, G, cols);
 }
 void launch_tr_keep_r(double* M, int64_t ldm, int wdt, cudaStream_t st) {
   k_tr_keep_r<<<tr_grid((int64_t)wdt * wdt), 256, 0, st>>>(M, ldm, wdt);
