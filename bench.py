@@ -11,8 +11,23 @@ One step = one full solve (init + 200 iterations) from HBM-resident inputs.
 Timing: W untimed warm-up solves, then K solves timed with CUDA events inside
 the library (whole solve, on its stream); inputs (CSR 1.07 GB + 108 GB of
 bases per solve) are far larger than the 126 MB L2. value = iterations / s
-(max over ranks). e2e = the same metric through sk_factorized_cg with host
-buffers (host validation + transposition + H2D + solve + D2H of history and core).
+(max over ranks).
+
+End-to-end legs (rank 0, N = 1), all through the C-ABI entry point a reference caller
+binds (sk_factorized_cg / _cg_lyapunov / _bicgstab) with HOST buffers:
+  e2e                the headline: C1, C2 in ordinary pageable memory (as the reference's
+                     DenseMatrix holds them): host CSR validation + symmetry + stencil
+                     detection, H2D through pinned staging lanes, solve, D2H of history + core
+  e2e_pinned_inputs  the same with C1, C2 in page-locked memory (sk_host_alloc): direct DMA
+  e2e_with_factors   e2e plus V and W copied to the host, as the reference's by-value
+                     FactorizedSolution returns them (107 GB at config 5); one timed call
+
+roofline: per kernel class, algorithmic bytes (as executed) over the
+class's CUDA-event time against the measured HBM copy peak (MEASURED_PEAKS.json), or, for
+the one compute-bound class (the BiCGSTAB dense core image), FP64 flops against the DFMA
+peak measured in the same run (sk_measure_fp64_peak). The line's roofline object is the
+class with the largest share of the solve; whole_step_frac = sum of the classes' roofline
+times / the solve's device time.
 
 --gpus N > 1 (torchrun, one rank per GPU): CG / Lyapunov CG configs run the
 row-partitioned solve over NCCL -- each rank holds 1/N of the rows
@@ -20,10 +35,12 @@ of A, B and the bases; per iteration two chunk-node all-gathers and one halo
 exchange; the same total problem at every N ("scaling": "strong"), value = the
 solve's iterations / s (max over ranks). BiCGSTAB configs run N replicas.
 
---impl reference: the reference's algorithm on the host cores (the reference
-itself cannot be built here -- Eigen3/GTest/vendor headers absent -- so its C
-restatement in oracle/, reference-order mode, parallel SpMM), on a bounded
-sample (first --cpu-iters iterations) of the same workload.
+cpu_baseline / --impl reference: the reference's algorithm on the host cores (the
+reference itself cannot be built here -- Eigen3/GTest/vendor headers absent -- so its C
+restatement in oracle/, reference-order mode): iterations 2 .. N+1 of the same workload
+(the solve window of an (N+1)-iteration run minus that of a 1-iteration run, so basis
+init is excluded); serial for cpu_baseline (the reference's default), SpMM threaded over
+all host cores for --impl reference (parallel.cpp). Host CPU model and nproc are printed.
 """
 from __future__ import annotations
 

@@ -747,7 +747,7 @@ struct GramSplit {
   static constexpr int MINB = H == 2 ? 2 : (S <= 4 ? 3 : 1);  // CTAs per SM (register budget)
 };
 #ifndef SK_GRAM_RING
-#define SK_GRAM_RING 1
+#define SK_GRAM_RING 0  // cp.async row ring: measured slower at config 4 (20.2 s vs 17.0 s), kept for reference
 #endif
 #ifndef SK_GRAM_STAGES
 #define SK_GRAM_STAGES 3
@@ -1420,6 +1420,18 @@ __global__ void __launch_bounds__(kFusedThreads, kWaveBlocks)
 #ifndef SK_CS_TMA
 #define SK_CS_TMA 1
 #endif
+#ifndef SK_CS_ROLEMAP
+#define SK_CS_ROLEMAP 0  // reducer warps on one scheduler (needs SK_CS_NC == 2)
+#endif
+#ifndef SK_CS_NOINLINE_RED
+#define SK_CS_NOINLINE_RED 1  // reducer warps call separately compiled (noinline) functions
+#endif
+#ifndef SK_CS_FAST
+#define SK_CS_FAST 1  // V2: branch-free interior steps of the column warps, three per loop trip
+#endif
+#ifndef SK_CS_V2
+#define SK_CS_V2 1  // software-pipelined steps, split-phase step barrier (needs SK_CS_TMA, SK_CS_CARRY)
+#endif
 constexpr int kCsNC = SK_CS_NC;            // grid columns per column thread
 constexpr int kCsColWarps = 16 / kCsNC;    // 512 columns
 constexpr int kCsRedWarps = 3;             // self-Gram, raw Gram slot 0, slot 1
@@ -1529,6 +1541,64 @@ __device__ __forceinline__ void cs_line_nodes(const double* __restrict__ gs, int
     }
   }
 }
+// Reducer warps of the column sweep as separately compiled functions: inside the kernel
+// (168 registers, three roles) ptxas sank every shared-memory load of these loops to its
+// first use, so a line cost 16 dependent shared-memory round trips and the reducer warps
+// were the critical path of every step (ncu, profiles/r2). Here the lane's 16 rows are
+// loaded up front; the sums keep the R1 order (rows m = 0 .. 15 sequentially, then the xor
+// butterfly), bitwise as before.
+template <int S>
+__device__ __noinline__ void cs_reduce_self(const double* __restrict__ K1, double* __restrict__ out, int lane) {
+  constexpr int NS = S * (S + 1) / 2;
+  double vv[kLRows][S];
+#pragma unroll
+  for (int m = 0; m < kLRows; ++m) sw_get<S>(K1 + (lane + 32 * m) * S, vv[m]);
+  double acc[NS];
+#pragma unroll
+  for (int e = 0; e < NS; ++e) acc[e] = 0.0;
+#pragma unroll
+  for (int m = 0; m < kLRows; ++m) {
+    int e = 0;
+#pragma unroll
+    for (int u = 0; u < S; ++u)
+#pragma unroll
+      for (int t = 0; t <= u; ++t) {
+        acc[e] = __dadd_rn(acc[e], __dmul_rn(vv[m][t], vv[m][u]));
+        ++e;
+      }
+  }
+#pragma unroll
+  for (int e = 0; e < NS; ++e) {
+    const double r = butterfly(acc[e]);
+    if (lane == e) out[e] = r;
+  }
+}
+template <int S>
+__device__ __noinline__ void cs_reduce_slot(const double* __restrict__ src, const double* __restrict__ Z,
+                                            double* __restrict__ out, int lane) {
+  constexpr int NB = S * S;
+  double av[kLRows][S], z[kLRows][S];
+#pragma unroll
+  for (int m = 0; m < kLRows; ++m) {
+    sw_get<S>(src + (lane + 32 * m) * S, av[m]);
+    sw_get<S>(Z + (lane + 32 * m) * S, z[m]);
+  }
+  double acc[NB];
+#pragma unroll
+  for (int e = 0; e < NB; ++e) acc[e] = 0.0;
+#pragma unroll
+  for (int m = 0; m < kLRows; ++m)
+#pragma unroll
+    for (int u = 0; u < S; ++u)
+#pragma unroll
+      for (int t = 0; t < S; ++t) acc[u * S + t] = __dadd_rn(acc[u * S + t], __dmul_rn(av[m][t], z[m][u]));
+#pragma unroll
+  for (int e = 0; e < NB; ++e) {
+    const double r = butterfly(acc[e]);
+    if (lane == e) out[e] = r;
+  }
+}
+
 template <int S>
 __global__ void __launch_bounds__(kCsThreads, 1)
     k_lanczos_cols(const __grid_constant__ SolveConst c, int side0, int nranges) {
@@ -1570,7 +1640,19 @@ __global__ void __launch_bounds__(kCsThreads, 1)
     m1[threadIdx.x] = __ldcg(sc.mcoef + (k - 1) * NB + threadIdx.x);
     m0[threadIdx.x] = two ? __ldcg(sc.mcoef + (k - 2) * NB + threadIdx.x) : 0.0;
   }
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  // Roles by hardware warp id: warp w issues on scheduler (SMSP) w % 4. The three reducer
+  // warps sit together on SMSP 0 (hardware warps 0, 4, 8 -> roles 9, 10, 11) and the eight
+  // column warps plus the halo warp share SMSPs 1 - 3, three each: the reducers' long
+  // dependent FP64 chains then run beside each other instead of behind two column warps'
+  // streams (ncu, profiles/r2: the reducers were the critical path of every step).
+  const int lane = threadIdx.x & 31;
+#if SK_CS_ROLEMAP
+  const int hwarp = threadIdx.x >> 5;
+  const int warp = (hwarp & 3) == 0 ? kCsColWarps + 1 + (hwarp >> 2) : (hwarp >> 2) * 3 + (hwarp & 3) - 1;
+  static_assert(kCsColWarps == 8 && kCsThreads == 384, "role map assumes 8 column warps + halo + 3 reducers");
+#else
+  const int warp = threadIdx.x >> 5;
+#endif
   const int64_t gS = (int64_t)g * S;
   // column roles: column warp w, lane l owns x0 + 32 w + l + 256 c (c < kCsNC);
   // the halo warp's lanes 0..3 own x0-1, x0+512 (computed), x0-2, x0+513 (loaded)
@@ -1686,6 +1768,421 @@ __global__ void __launch_bounds__(kCsThreads, 1)
 #pragma unroll
     for (int t = 0; t < S; ++t) cup[q][t] = cce[q][t] = kup[q][t] = kce[q][t] = 0.0;
 #endif
+#if SK_CS_V2
+  // ---- software-pipelined steps with a split-phase step barrier ----------------------
+  // The step barrier is an mbarrier (one arrival per warp at the END of its step t,
+  // waited for only where step t + 1 first touches another warp's data), and a column
+  // warp's step is reordered so that nothing in its first half depends on other warps:
+  //   A-part(y): U_k(y) from operands already in registers (the thread's own column of
+  //              U_{k-1} is carried; its neighbours' and the U_{k-2} value were loaded
+  //              from the TMA rings during the previous step), global store, K ring store
+  //   wait(step t - 1 finished everywhere)
+  //   loads: K(y-1) neighbours AND the A-part operands of line y + 1 (their latency
+  //              overlaps the z-part)
+  //   z-part(y-1): z' = op U_k on line y - 1, Z ring store; arrive.
+  // Every point's arithmetic is unchanged (bitwise the barrier-per-line schedule).
+  __shared__ __align__(8) uint64_t sbar[2];
+  if (threadIdx.x < 2) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"((unsigned)__cvta_generic_to_shared(&sbar[threadIdx.x])),
+                 "r"((unsigned)(kCsThreads / 32))
+                 : "memory");
+  }
+  __syncthreads();
+  auto step_arrive = [&](int t) {
+    __syncwarp();
+    if (lane == 0)
+      asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(
+                       (unsigned)__cvta_generic_to_shared(&sbar[(t + 1) & 1]))
+                   : "memory");
+  };
+  auto step_wait = [&](int t) {  // all warps finished step t - 1 (t >= 1)
+    const unsigned par = (t & 1) ? (unsigned)(t >> 1) & 1u : (unsigned)((t >> 1) + 1) & 1u;
+    mb_wait(&sbar[t & 1], par);
+  };
+  double ale[kCsNC][S], ari[kCsNC][S], adn[kCsNC][S], abb[kCsNC][S];  // A-part operands of line y
+  auto load_a_ops = [&](int yy) {  // neighbours of U_{k-1}(yy), U_{k-1}(yy + 1) own, U_{k-2}(yy) own
+    const double* A0 = Ar + (yy & (kCsAR - 1)) * AL;
+    const double* Ap = Ar + ((yy + 1) & (kCsAR - 1)) * AL;
+    const double* B0 = Br + (yy & (kCsBR - 1)) * BL;
+#pragma unroll
+    for (int q = 0; q < kCsNC; ++q)
+      if (q < nslot) {
+        const int ai = (xs[q] - x0 + 2) * S;
+        sw_get<S>(A0 + ai - S, ale[q]);
+        sw_get<S>(A0 + ai + S, ari[q]);
+        sw_get<S>(Ap + ai, adn[q]);
+        sw_get<S>(B0 + ai + (BO - 2) * S, abb[q]);
+      }
+  };
+  if (warp <= kCsColWarps && compute) {
+    mb_wait(&mbar[0], 0u);  // group 0: U_{k-1} lines ys-3 .. ys+1, U_{k-2} line ys
+#pragma unroll
+    for (int q = 0; q < kCsNC; ++q)
+      if (q < nslot) {
+        const int ai = (xs[q] - x0 + 2) * S;
+        sw_get<S>(Ar + ((ys - 1) & (kCsAR - 1)) * AL + ai, cup[q]);
+        sw_get<S>(Ar + (ys & (kCsAR - 1)) * AL + ai, cce[q]);
+      }
+    load_a_ops(ys);
+  }
+#if SK_CS_FAST
+  // Interior steps of the column warps (lines y0+1 .. y1-1: every flag of the generic step
+  // is true, every point is in the grid), three per loop trip so that the three-deep
+  // register rotations (U_{k-1} own column: loaded -> centre -> up; U_k: new -> centre -> up)
+  // come back to their registers without moves; coefficients live in registers.
+  double rc5[5], rm0[NB], rm1[NB];
+  NF<S> rf1;
+#pragma unroll
+  for (int e = 0; e < 5; ++e) rc5[e] = sc.scoef[e];
+#pragma unroll
+  for (int e = 0; e < NB; ++e) {
+    rm0[e] = m0[e];
+    rm1[e] = m1[e];
+  }
+  rf1 = f1s;
+  const int ai0 = warp < kCsColWarps ? (xs[0] - x0 + 2) * S : 0, ki0 = ai0 - S, zi0 = ai0 - 2 * S;
+  constexpr int QO = (kSeg / kCsNC) * S;  // doubles between a thread's columns
+  double* pU = UK + ((int64_t)(y0 + 1) * g + (warp < kCsColWarps ? xs[0] : 0)) * S;
+  auto main_step = [&](int y) {
+    const int t = y - ys;
+    double vq[kCsNC][S];
+    {
+      double* K0 = Kb + (y & (kCsKR - 1)) * KL + ki0;
+#pragma unroll
+      for (int q = 0; q < kCsNC; ++q) {
+        double z[S], v[S], ce[S];
+#pragma unroll
+        for (int u = 0; u < S; ++u) ce[u] = cce[q][u];
+        cs_stencil<S>(rc5, cup[q], ale[q], ce, ari[q], adn[q], z);
+#pragma unroll
+        for (int u = 0; u < S; ++u) {
+          cup[q][u] = ce[u];
+          cce[q][u] = adn[q][u];
+        }
+        norm_row<S>(z, rf1, v);
+        if (two) {
+#pragma unroll
+          for (int u = 0; u < S; ++u) {
+            double tmp = 0.0;
+#pragma unroll
+            for (int w_ = 0; w_ < S; ++w_) tmp = __dadd_rn(tmp, __dmul_rn(abb[q][w_], rm0[u * S + w_]));
+            v[u] = __dsub_rn(v[u], tmp);
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < S; ++u) {
+          double tmp = 0.0;
+#pragma unroll
+          for (int w_ = 0; w_ < S; ++w_) tmp = __dadd_rn(tmp, __dmul_rn(ce[w_], rm1[u * S + w_]));
+          v[u] = __dsub_rn(v[u], tmp);
+        }
+        st_row<S>(pU + q * QO, 0, v);
+        sw_put<S>(K0 + q * QO, v);
+#pragma unroll
+        for (int u = 0; u < S; ++u) vq[q][u] = v[u];
+      }
+      pU += gS;
+    }
+    step_wait(t);
+    {
+      const double* K1 = Kb + ((y - 1) & (kCsKR - 1)) * KL + ki0;
+      double kle[kCsNC][S], kri[kCsNC][S];
+#pragma unroll
+      for (int q = 0; q < kCsNC; ++q) {
+        sw_get<S>(K1 + q * QO - S, kle[q]);
+        sw_get<S>(K1 + q * QO + S, kri[q]);
+      }
+      mb_wait(&mbar[(t + 1) & 7], (unsigned)((t + 1) >> 3) & 1u);
+      {
+        const double* A0 = Ar + ((y + 1) & (kCsAR - 1)) * AL + ai0;
+        const double* Ap = Ar + ((y + 2) & (kCsAR - 1)) * AL + ai0;
+        const double* B0 = Br + ((y + 1) & (kCsBR - 1)) * BL + ai0 + (BO - 2) * S;
+#pragma unroll
+        for (int q = 0; q < kCsNC; ++q) {
+          sw_get<S>(A0 + q * QO - S, ale[q]);
+          sw_get<S>(A0 + q * QO + S, ari[q]);
+          sw_get<S>(Ap + q * QO, adn[q]);
+          sw_get<S>(B0 + q * QO, abb[q]);
+        }
+      }
+      double* Z1 = Zs + ((y - 1) & 1) * ZL + zi0;
+#pragma unroll
+      for (int q = 0; q < kCsNC; ++q) {
+        double z2[S];
+#pragma unroll
+        for (int u = 0; u < S; ++u) {
+          double a2 = __dadd_rn(0.0, __dmul_rn(rc5[0], kup[q][u]));
+          a2 = __dadd_rn(a2, __dmul_rn(rc5[1], kle[q][u]));
+          a2 = __dadd_rn(a2, __dmul_rn(rc5[2], kce[q][u]));
+          a2 = __dadd_rn(a2, __dmul_rn(rc5[3], kri[q][u]));
+          z2[u] = __dadd_rn(a2, __dmul_rn(rc5[4], vq[q][u]));
+          kup[q][u] = kce[q][u];
+          kce[q][u] = vq[q][u];
+        }
+        sw_put<S>(Z1 + q * QO, z2);
+      }
+    }
+    step_arrive(t);
+  };
+  // The halo warp's interior step: its two computing lanes form U_k at columns x0 - 1 and
+  // x0 + 512 for the neighbours' stencils (K ring only: no global store, and z' is never
+  // needed there, so there is no z-part).
+  const int hai = (xs[0] - x0 + 2) * S;
+  auto halo_step = [&](int y) {
+    const int t = y - ys;
+    if (compute) {
+      double z[S], v[S], ce[S];
+#pragma unroll
+      for (int u = 0; u < S; ++u) ce[u] = cce[0][u];
+      cs_stencil<S>(rc5, cup[0], ale[0], ce, ari[0], adn[0], z);
+#pragma unroll
+      for (int u = 0; u < S; ++u) {
+        cup[0][u] = ce[u];
+        cce[0][u] = adn[0][u];
+      }
+      norm_row<S>(z, rf1, v);
+      if (two) {
+#pragma unroll
+        for (int u = 0; u < S; ++u) {
+          double tmp = 0.0;
+#pragma unroll
+          for (int w_ = 0; w_ < S; ++w_) tmp = __dadd_rn(tmp, __dmul_rn(abb[0][w_], rm0[u * S + w_]));
+          v[u] = __dsub_rn(v[u], tmp);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < S; ++u) {
+        double tmp = 0.0;
+#pragma unroll
+        for (int w_ = 0; w_ < S; ++w_) tmp = __dadd_rn(tmp, __dmul_rn(ce[w_], rm1[u * S + w_]));
+        v[u] = __dsub_rn(v[u], tmp);
+      }
+      if (!cv[0]) {
+#pragma unroll
+        for (int u = 0; u < S; ++u) v[u] = 0.0;
+      }
+      sw_put<S>(Kb + (y & (kCsKR - 1)) * KL + hai - S, v);
+#pragma unroll
+      for (int u = 0; u < S; ++u) {
+        kup[0][u] = kce[0][u];
+        kce[0][u] = v[u];
+      }
+    }
+    step_wait(t);
+    if (compute) {
+      mb_wait(&mbar[(t + 1) & 7], (unsigned)((t + 1) >> 3) & 1u);
+      const double* A0 = Ar + ((y + 1) & (kCsAR - 1)) * AL + hai;
+      sw_get<S>(A0 - S, ale[0]);
+      sw_get<S>(A0 + S, ari[0]);
+      sw_get<S>(Ar + ((y + 2) & (kCsAR - 1)) * AL + hai, adn[0]);
+      sw_get<S>(Br + ((y + 1) & (kCsBR - 1)) * BL + hai + (BO - 2) * S, abb[0]);
+    }
+    step_arrive(t);
+  };
+  // The reducer warps' interior step (lines y-1 / y-2 inside the range, the prefetched lines
+  // y+5 / y+4 inside the grid): wait, one lean bulk-copy issue by the issuer's lane 0, one
+  // call of the separately compiled reduction, arrive.
+  const int rrole = warp - kCsColWarps - 1;  // 0: self-Gram (and issuer), 1 / 2: raw-Gram slots
+  const unsigned ring_dst = (unsigned)((ca - x0 + 2) * S);
+  auto red_step = [&](int y) {
+    const int t = y - ys;
+    step_wait(t);
+    if (rrole == 0) {
+      if (lane == 0) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        uint64_t* mb = &mbar[(t + 4) & 7];
+        mb_expect_arrive(mb, two ? 2u * lbytes : lbytes);
+        bulk_g2s(Ar + ((y + 5) & (kCsAR - 1)) * AL + ring_dst, U1 + ((int64_t)(y + 5) * g + ca) * S, lbytes, mb);
+        if (two)
+          bulk_g2s(Br + ((y + 4) & (kCsBR - 1)) * BL + ring_dst, U0 + ((int64_t)(y + 4) * g + ca) * S, lbytes, mb);
+      }
+      const int yl = y - 1;
+      cs_reduce_self<S>(Kb + (yl & (kCsKR - 1)) * KL + S, gseg + ((int64_t)yl * nstrip + sx) * NE, lane);
+    } else {
+      const int yl = y - 2;
+      cs_reduce_slot<S>(rrole == 1 ? Ar + (yl & (kCsAR - 1)) * AL + 2 * S : Kb + (yl & (kCsKR - 1)) * KL + S,
+                        Zs + (yl & 1) * ZL, gseg + ((int64_t)yl * nstrip + sx) * NE + NS + (rrole - 1) * NB, lane);
+    }
+    step_arrive(t);
+  };
+#endif
+  for (int y = ys; y <= y1 + 1; ++y) {
+    const int t = y - ys;
+#if SK_CS_FAST
+    // reducers: y-2 >= y0, y-1 < y1, and the issued lines y+5, y+4 in [0, g)
+    if (warp > kCsColWarps && y >= y0 + 2 && y <= y1 - 1 && y + 5 < g && y + 4 >= 0 && y + 4 <= y1 + 1) {
+      red_step(y);
+      continue;
+    }
+    if (warp <= kCsColWarps && y >= y0 + 1 && y + 2 <= y1 - 1) {
+      if (warp < kCsColWarps) {
+        main_step(y);
+        main_step(y + 1);
+        main_step(y + 2);
+      } else {
+        halo_step(y);
+        halo_step(y + 1);
+        halo_step(y + 2);
+      }
+      y += 2;
+      continue;
+    }
+#endif
+    if (warp <= kCsColWarps) {
+      const bool act = compute && y <= y1;
+      double vq[kCsNC][S];
+      if (act) {
+        double* K0 = Kb + (y & (kCsKR - 1)) * KL;
+        const bool wr = inner && y >= y0 && y < y1;
+#pragma unroll
+        for (int q = 0; q < kCsNC; ++q)
+          if (q < nslot) {
+            const int ki = (xs[q] - x0 + 1) * S;
+            double z[S], v[S], ce[S];
+#pragma unroll
+            for (int u = 0; u < S; ++u) ce[u] = cce[q][u];
+            cs_stencil<S>(sc.scoef, cup[q], ale[q], ce, ari[q], adn[q], z);
+#pragma unroll
+            for (int u = 0; u < S; ++u) {
+              cup[q][u] = ce[u];
+              cce[q][u] = adn[q][u];
+            }
+            norm_row<S>(z, f1s, v);
+            if (two) {
+#pragma unroll
+              for (int u = 0; u < S; ++u) {
+                double tmp = 0.0;
+#pragma unroll
+                for (int w_ = 0; w_ < S; ++w_) tmp = __dadd_rn(tmp, __dmul_rn(abb[q][w_], m0[u * S + w_]));
+                v[u] = __dsub_rn(v[u], tmp);
+              }
+            }
+#pragma unroll
+            for (int u = 0; u < S; ++u) {
+              double tmp = 0.0;
+#pragma unroll
+              for (int w_ = 0; w_ < S; ++w_) tmp = __dadd_rn(tmp, __dmul_rn(ce[w_], m1[u * S + w_]));
+              v[u] = __dsub_rn(v[u], tmp);
+            }
+            if (!(cv[q] && y >= 0 && y < g)) {
+#pragma unroll
+              for (int u = 0; u < S; ++u) v[u] = 0.0;
+            }
+            if (wr) st_row<S>(UK + ((int64_t)y * g + xs[q]) * S, 0, v);
+            sw_put<S>(K0 + ki, v);
+#pragma unroll
+            for (int u = 0; u < S; ++u) vq[q][u] = v[u];
+          }
+      }
+      if (t > 0) step_wait(t);
+      if (act) {
+        const double* K1 = Kb + ((y - 1) & (kCsKR - 1)) * KL;
+        double* Z1 = Zs + ((y - 1) & 1) * ZL;
+        const bool zl = inner && y - 1 >= y0 && y - 1 < y1;
+        double kle[kCsNC][S], kri[kCsNC][S];
+#pragma unroll
+        for (int q = 0; q < kCsNC; ++q)
+          if (q < nslot) {
+            const int ki = (xs[q] - x0 + 1) * S;
+            sw_get<S>(K1 + ki - S, kle[q]);
+            sw_get<S>(K1 + ki + S, kri[q]);
+          }
+        if (y + 1 <= y1) {
+          mb_wait(&mbar[(t + 1) & 7], (unsigned)((t + 1) >> 3) & 1u);  // lines y + 2 (U_{k-1}), y + 1 (U_{k-2})
+          load_a_ops(y + 1);
+        }
+#pragma unroll
+        for (int q = 0; q < kCsNC; ++q)
+          if (q < nslot) {
+            double z2[S];
+#pragma unroll
+            for (int u = 0; u < S; ++u) {
+              double a2 = __dadd_rn(0.0, __dmul_rn(sc.scoef[0], kup[q][u]));
+              a2 = __dadd_rn(a2, __dmul_rn(sc.scoef[1], kle[q][u]));
+              a2 = __dadd_rn(a2, __dmul_rn(sc.scoef[2], kce[q][u]));
+              a2 = __dadd_rn(a2, __dmul_rn(sc.scoef[3], kri[q][u]));
+              z2[u] = __dadd_rn(a2, __dmul_rn(sc.scoef[4], vq[q][u]));
+              kup[q][u] = kce[q][u];
+              kce[q][u] = vq[q][u];
+            }
+            if (zl) sw_put<S>(Z1 + (xs[q] - x0) * S, z2);
+          }
+      }
+    } else {
+      if (t > 0) step_wait(t);
+      // group t + 4: U_{k-1} line y + 5, U_{k-2} line y + 4 (consumed from step t + 3 on; the
+      // slots' last readers finished step t - 1)
+      if (issuer && y + 4 <= y1 + 1) issue(t + 4, y + 5, y + 5, y + 4);
+      const int r = warp - kCsColWarps - 1;
+#if SK_CS_NOINLINE_RED
+      if (r == 0) {
+        const int yl = y - 1;
+        if (yl >= y0 && yl < y1)
+          cs_reduce_self<S>(Kb + (yl & (kCsKR - 1)) * KL + S, gseg + ((int64_t)yl * nstrip + sx) * NE, lane);
+      } else {
+        const int yl = y - 2;
+        if (yl >= y0 && yl < y1)
+          cs_reduce_slot<S>(r == 1 ? Ar + (yl & (kCsAR - 1)) * AL + 2 * S : Kb + (yl & (kCsKR - 1)) * KL + S,
+                            Zs + (yl & 1) * ZL, gseg + ((int64_t)yl * nstrip + sx) * NE + NS + (r - 1) * NB, lane);
+      }
+#else
+      if (r == 0) {
+        const int yl = y - 1;
+        if (yl >= y0 && yl < y1) {
+          const double* K1 = Kb + (yl & (kCsKR - 1)) * KL + S;
+          double acc[NS];
+#pragma unroll
+          for (int e = 0; e < NS; ++e) acc[e] = 0.0;
+#pragma unroll 4
+          for (int m = 0; m < kLRows; ++m) {
+            double vv[S];
+            sw_get<S>(K1 + (lane + 32 * m) * S, vv);
+            int e = 0;
+#pragma unroll
+            for (int u = 0; u < S; ++u)
+#pragma unroll
+              for (int w_ = 0; w_ <= u; ++w_) {
+                acc[e] = __dadd_rn(acc[e], __dmul_rn(vv[w_], vv[u]));
+                ++e;
+              }
+          }
+#pragma unroll
+          for (int e = 0; e < NS; ++e) {
+            const double vv = butterfly(acc[e]);
+            if (lane == e) gseg[((int64_t)yl * nstrip + sx) * NE + e] = vv;
+          }
+        }
+      } else {
+        const int yl = y - 2;
+        if (yl >= y0 && yl < y1) {
+          const double* src = r == 1 ? Ar + (yl & (kCsAR - 1)) * AL + 2 * S : Kb + (yl & (kCsKR - 1)) * KL + S;
+          const double* Z = Zs + (yl & 1) * ZL;
+          double acc[NB];
+#pragma unroll
+          for (int e = 0; e < NB; ++e) acc[e] = 0.0;
+#pragma unroll 4
+          for (int m = 0; m < kLRows; ++m) {
+            const int cl = lane + 32 * m;
+            double av[S], z[S];
+            sw_get<S>(src + cl * S, av);
+            sw_get<S>(Z + cl * S, z);
+#pragma unroll
+            for (int u = 0; u < S; ++u)
+#pragma unroll
+              for (int w_ = 0; w_ < S; ++w_) acc[u * S + w_] = __dadd_rn(acc[u * S + w_], __dmul_rn(av[w_], z[u]));
+          }
+#pragma unroll
+          for (int e = 0; e < NB; ++e) {
+            const double vv = butterfly(acc[e]);
+            if (lane == e) gseg[((int64_t)yl * nstrip + sx) * NE + NS + (r - 1) * NB + e] = vv;
+          }
+        }
+      }
+#endif
+    }
+    step_arrive(t);
+  }
+#else
 #ifdef SK_CS_PROF2
   long long pf_wait = 0, pf_work = 0, pf_mb = 0, pf_a = clock64();
 #endif
@@ -1830,7 +2327,21 @@ __global__ void __launch_bounds__(kCsThreads, 1)
     } else {
       // reducer warps (R1 lane order): self-Gram of line y-1, raw Grams of line y-2
       const int r = warp - kCsColWarps - 1;
+#if SK_CS_NOINLINE_RED
       if (r == 0) {
+        const int yl = y - 1;
+        if (yl >= y0 && yl < y1)
+          cs_reduce_self<S>(Kb + (yl & (kCsKR - 1)) * KL + S, gseg + ((int64_t)yl * nstrip + sx) * NE, lane);
+      } else if (y - 2 >= y0 && y - 2 < y1) {
+        const int yl = y - 2;
+        cs_reduce_slot<S>(r == 1 ? Ar + (yl & (kCsAR - 1)) * AL + 2 * S : Kb + (yl & (kCsKR - 1)) * KL + S,
+                          Zs + (yl & 1) * ZL, gseg + ((int64_t)yl * nstrip + sx) * NE + NS + (r - 1) * NB, lane);
+      }
+      if (true) {  // (the inline loops below are the SK_CS_NOINLINE_RED=0 variant)
+      } else if (r == 0) {
+#else
+      if (r == 0) {
+#endif
         const int yl = y - 1;
         if (yl >= y0 && yl < y1) {
           const double* K1 = Kb + (yl & (kCsKR - 1)) * KL + S;
@@ -1889,7 +2400,15 @@ __global__ void __launch_bounds__(kCsThreads, 1)
     pf_work += pf_a - pf_b;
 #endif
   }
-#ifdef SK_CS_PROF2
+#endif  // SK_CS_V2
+#if SK_CS_V2
+  // every bulk copy issued must have landed before the tail reuses the rings
+  if (issuer) {
+    const int T = y1 + 2 - ys;
+    for (int j = T - 4; j < T; ++j) mb_wait(&mbar[j & 7], (unsigned)(j >> 3) & 1u);
+  }
+#endif
+#if defined(SK_CS_PROF2) && !SK_CS_V2
   if (lane == 0 && blockIdx.x == 5 && side == 0 && (k == 100 || k == 101))
     printf("CSW2 k %lld warp %d steps %d wait %lld (mbarrier %lld) work %lld\n", (long long)k, warp, y1 + 2 - ys,
            pf_wait, pf_mb, pf_work);
