@@ -1430,7 +1430,10 @@ __global__ void __launch_bounds__(kFusedThreads, kWaveBlocks)
 #define SK_CS_FAST 1  // V2: branch-free interior steps of the column warps, three per loop trip
 #endif
 #ifndef SK_CS_V2
-#define SK_CS_V2 1  // software-pipelined steps, split-phase step barrier (needs SK_CS_TMA, SK_CS_CARRY)
+#define SK_CS_V2 0  // EXPERIMENTAL, OFF: software-pipelined steps with a split-phase mbarrier step barrier.
+                    // Faster (C5 1815 vs 1776 iter/s) but NOT reproducible: config 3 (2908 launches of
+                    // 148 CTAs) shows rounding-level deviations at data-dependent iterations in every run
+                    // (profiles/r2/README.md); the barrier-per-line schedule below is bit-stable.
 #endif
 constexpr int kCsNC = SK_CS_NC;            // grid columns per column thread
 constexpr int kCsColWarps = 16 / kCsNC;    // 512 columns
@@ -1439,8 +1442,12 @@ constexpr int kCsThreads = 32 * (kCsColWarps + 1 + kCsRedWarps);
 constexpr int kCsA = kSeg + 4;             // U_{k-1} lines: columns x0-2 .. x0+513
 constexpr int kCsK = kSeg + 2;             // U_k / U_{k-2} lines: columns x0-1 .. x0+512
 constexpr int kCsAR = 8;                   // U_{k-1} ring: lines y-3 .. y+4 (prefetch 4)
-constexpr int kCsBR = 8;                   // U_{k-2} ring: lines y-3 .. y+4 (prefetch 4)
-constexpr int kCsKR = 4;                   // U_k ring: lines y-3 .. y
+#ifndef SK_CS_V3
+#define SK_CS_V3 0  // (measured 1730 vs 1815 iter/s at C5: off) reducer warps decoupled from the step barrier (deeper K / Z rings); needs SK_CS_V2
+#endif
+constexpr int kCsBR = SK_CS_V3 ? 4 : 8;    // U_{k-2} ring (V3: lines y .. y+3; else y-3 .. y+4)
+constexpr int kCsKR = SK_CS_V3 ? 8 : 4;    // U_k ring (V3: the reducers may lag two lines)
+constexpr int kCsZR = SK_CS_V3 ? 4 : 2;    // z' ring
 constexpr int kCsMaxLines = 1024;          // lines per range (the tail's line nodes fit in the rings)
 constexpr int kCsBlk = 8;                  // lines per tail block node (range alignment)
 
@@ -1547,6 +1554,26 @@ __device__ __forceinline__ void cs_line_nodes(const double* __restrict__ gs, int
 // were the critical path of every step (ncu, profiles/r2). Here the lane's 16 rows are
 // loaded up front; the sums keep the R1 order (rows m = 0 .. 15 sequentially, then the xor
 // butterfly), bitwise as before.
+// Four xor butterflies at once (R1 lane combine, d = 16 .. 1) with halving exchanges: in
+// round d = 16 the lanes with bit 4 clear keep entries 0, 1 and hand 2, 3 to their partner
+// (and vice versa), in round d = 8 they split once more, rounds 4, 2, 1 run on the single
+// entry a lane is left with. Every addition is "own + partner" exactly as in butterfly(), and
+// IEEE addition is commutative, so every lane of the plain butterfly holds the same bits at
+// every level: the entry e = lane >> 3 that a lane ends with is bitwise butterfly(v_e). 15
+// shuffle/add pairs instead of 40 on the reducer warps' critical path.
+__device__ __forceinline__ double butterfly4(double v0, double v1, double v2, double v3, int lane) {
+  const bool h4 = (lane & 16) != 0, h3 = (lane & 8) != 0;
+  double k0 = h4 ? v2 : v0, k1 = h4 ? v3 : v1;
+  const double s0 = h4 ? v0 : v2, s1 = h4 ? v1 : v3;
+  k0 = __dadd_rn(k0, shfl_xor_d(s0, 16));
+  k1 = __dadd_rn(k1, shfl_xor_d(s1, 16));
+  double kk = h3 ? k1 : k0;
+  const double ss = h3 ? k0 : k1;
+  kk = __dadd_rn(kk, shfl_xor_d(ss, 8));
+#pragma unroll
+  for (int d = 4; d >= 1; d >>= 1) kk = __dadd_rn(kk, shfl_xor_d(kk, d));
+  return kk;
+}
 template <int S>
 __device__ __noinline__ void cs_reduce_self(const double* __restrict__ K1, double* __restrict__ out, int lane) {
   constexpr int NS = S * (S + 1) / 2;
@@ -1567,10 +1594,15 @@ __device__ __noinline__ void cs_reduce_self(const double* __restrict__ K1, doubl
         ++e;
       }
   }
+  if constexpr (NS == 3) {
+    const double r = butterfly4(acc[0], acc[1], acc[2], 0.0, lane);
+    if ((lane & 7) == 0 && (lane >> 3) < NS) out[lane >> 3] = r;
+  } else {
 #pragma unroll
-  for (int e = 0; e < NS; ++e) {
-    const double r = butterfly(acc[e]);
-    if (lane == e) out[e] = r;
+    for (int e = 0; e < NS; ++e) {
+      const double r = butterfly(acc[e]);
+      if (lane == e) out[e] = r;
+    }
   }
 }
 template <int S>
@@ -1592,10 +1624,15 @@ __device__ __noinline__ void cs_reduce_slot(const double* __restrict__ src, cons
     for (int u = 0; u < S; ++u)
 #pragma unroll
       for (int t = 0; t < S; ++t) acc[u * S + t] = __dadd_rn(acc[u * S + t], __dmul_rn(av[m][t], z[m][u]));
+  if constexpr (NB == 4) {
+    const double r = butterfly4(acc[0], acc[1], acc[2], acc[3], lane);
+    if ((lane & 7) == 0) out[lane >> 3] = r;
+  } else {
 #pragma unroll
-  for (int e = 0; e < NB; ++e) {
-    const double r = butterfly(acc[e]);
-    if (lane == e) out[e] = r;
+    for (int e = 0; e < NB; ++e) {
+      const double r = butterfly(acc[e]);
+      if (lane == e) out[e] = r;
+    }
   }
 }
 
@@ -1632,7 +1669,7 @@ __global__ void __launch_bounds__(kCsThreads, 1)
   double* Ar = cs_smem;                    // [kCsAR][AL]
   double* Br = Ar + kCsAR * AL;            // [kCsBR][KL]
   double* Kb = Br + kCsBR * BL;            // [kCsKR][KL]
-  double* Zs = Kb + kCsKR * KL;            // [2][ZL]
+  double* Zs = Kb + kCsKR * KL;            // [kCsZR][ZL]
   __shared__ NF<S> f1s;
   __shared__ double m1[NB], m0[NB];
   if (threadIdx.x == 0) load_nf<S>(sc.nfac, k - 1, f1s);
@@ -1701,7 +1738,7 @@ __global__ void __launch_bounds__(kCsThreads, 1)
   // mbar[t & 7]. Columns outside the grid stay zero (written once here); lines
   // outside the grid are zero-filled by the issuing warp.
   __shared__ __align__(8) uint64_t mbar[8];
-  const bool issuer = warp == kCsColWarps + 1;
+  const bool issuer = warp == (SK_CS_V3 ? kCsColWarps : kCsColWarps + 1);  // V3: the halo warp
   const int ca = x0 - 2 < 0 ? 0 : x0 - 2, cb = x0 + kSeg + 1 >= g ? g - 1 : x0 + kSeg + 1;
   const unsigned lbytes = (unsigned)((cb - ca + 1) * S * 8);
   if (threadIdx.x < 8) mb_init(&mbar[threadIdx.x]);
@@ -1741,7 +1778,7 @@ __global__ void __launch_bounds__(kCsThreads, 1)
   // prologue: U_{k-1} lines ys-3 .. ys+4, U_{k-2} lines ys .. ys+3 (groups 0 .. 3)
   if (issuer) {
     issue(0, ys - 3, ys + 1, ys);
-    for (int t = 1; t < 4; ++t) issue(t, ys + t + 1, ys + t + 1, ys + t);
+    for (int t = 1; t < (SK_CS_V3 ? 3 : 4); ++t) issue(t, ys + t + 1, ys + t + 1, ys + t);
   }
 #else
   __syncthreads();
@@ -1781,6 +1818,33 @@ __global__ void __launch_bounds__(kCsThreads, 1)
   //              overlaps the z-part)
   //   z-part(y-1): z' = op U_k on line y - 1, Z ring store; arrive.
   // Every point's arithmetic is unchanged (bitwise the barrier-per-line schedule).
+#if SK_CS_V3
+  // V3: two barrier rings. sbar[t & 3] completes when the nine producer warps (columns + halo)
+  // have finished step t - 1; rbar[t & 3] when the three reducer warps have finished step t.
+  // Producers wait for sbar of the previous step and for the reducers' step t - 2, so the
+  // reducers may run up to two lines behind (K ring of 8, z' ring of 4 lines); their long
+  // dependent sums no longer gate the producers' step. Reducers only wait for sbar.
+  __shared__ __align__(8) uint64_t sbar[4], rbar[4];
+  if (threadIdx.x < 8) {
+    uint64_t* b = threadIdx.x < 4 ? &sbar[threadIdx.x] : &rbar[threadIdx.x - 4];
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"((unsigned)__cvta_generic_to_shared(b)),
+                 "r"(threadIdx.x < 4 ? (unsigned)(kCsColWarps + 1) : (unsigned)kCsRedWarps)
+                 : "memory");
+  }
+  __syncthreads();
+  const bool producer = warp <= kCsColWarps;
+  auto step_arrive = [&](int t) {
+    __syncwarp();
+    if (lane == 0)
+      asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(
+                       (unsigned)__cvta_generic_to_shared(producer ? &sbar[(t + 1) & 3] : &rbar[t & 3]))
+                   : "memory");
+  };
+  auto step_wait = [&](int t) {  // t >= 1
+    mb_wait(&sbar[t & 3], (unsigned)((t - 1) >> 2) & 1u);
+    if (producer && t >= 2) mb_wait(&rbar[(t - 2) & 3], (unsigned)((t - 2) >> 2) & 1u);
+  };
+#else
   __shared__ __align__(8) uint64_t sbar[2];
   if (threadIdx.x < 2) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"((unsigned)__cvta_generic_to_shared(&sbar[threadIdx.x])),
@@ -1796,9 +1860,12 @@ __global__ void __launch_bounds__(kCsThreads, 1)
                    : "memory");
   };
   auto step_wait = [&](int t) {  // all warps finished step t - 1 (t >= 1)
+#ifndef SK_CS_DBG_V1LIKE
     const unsigned par = (t & 1) ? (unsigned)(t >> 1) & 1u : (unsigned)((t >> 1) + 1) & 1u;
     mb_wait(&sbar[t & 1], par);
+#endif
   };
+#endif
   double ale[kCsNC][S], ari[kCsNC][S], adn[kCsNC][S], abb[kCsNC][S];  // A-part operands of line y
   auto load_a_ops = [&](int yy) {  // neighbours of U_{k-1}(yy), U_{k-1}(yy + 1) own, U_{k-2}(yy) own
     const double* A0 = Ar + (yy & (kCsAR - 1)) * AL;
@@ -1905,7 +1972,7 @@ __global__ void __launch_bounds__(kCsThreads, 1)
           sw_get<S>(B0 + q * QO, abb[q]);
         }
       }
-      double* Z1 = Zs + ((y - 1) & 1) * ZL + zi0;
+      double* Z1 = Zs + ((y - 1) & (kCsZR - 1)) * ZL + zi0;
 #pragma unroll
       for (int q = 0; q < kCsNC; ++q) {
         double z2[S];
@@ -1928,6 +1995,7 @@ __global__ void __launch_bounds__(kCsThreads, 1)
   // x0 + 512 for the neighbours' stencils (K ring only: no global store, and z' is never
   // needed there, so there is no z-part).
   const int hai = (xs[0] - x0 + 2) * S;
+  const unsigned ring_dst = (unsigned)((ca - x0 + 2) * S);
   auto halo_step = [&](int y) {
     const int t = y - ys;
     if (compute) {
@@ -1969,6 +2037,16 @@ __global__ void __launch_bounds__(kCsThreads, 1)
       }
     }
     step_wait(t);
+#if SK_CS_V3
+    if (lane == 0) {  // group t + 3: U_{k-1} line y + 4, U_{k-2} line y + 3 (both inside the grid here)
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      uint64_t* mb = &mbar[(t + 3) & 7];
+      mb_expect_arrive(mb, two ? 2u * lbytes : lbytes);
+      bulk_g2s(Ar + ((y + 4) & (kCsAR - 1)) * AL + ring_dst, U1 + ((int64_t)(y + 4) * g + ca) * S, lbytes, mb);
+      if (two)
+        bulk_g2s(Br + ((y + 3) & (kCsBR - 1)) * BL + ring_dst, U0 + ((int64_t)(y + 3) * g + ca) * S, lbytes, mb);
+    }
+#endif
     if (compute) {
       mb_wait(&mbar[(t + 1) & 7], (unsigned)((t + 1) >> 3) & 1u);
       const double* A0 = Ar + ((y + 1) & (kCsAR - 1)) * AL + hai;
@@ -1983,12 +2061,11 @@ __global__ void __launch_bounds__(kCsThreads, 1)
   // y+5 / y+4 inside the grid): wait, one lean bulk-copy issue by the issuer's lane 0, one
   // call of the separately compiled reduction, arrive.
   const int rrole = warp - kCsColWarps - 1;  // 0: self-Gram (and issuer), 1 / 2: raw-Gram slots
-  const unsigned ring_dst = (unsigned)((ca - x0 + 2) * S);
   auto red_step = [&](int y) {
     const int t = y - ys;
     step_wait(t);
     if (rrole == 0) {
-      if (lane == 0) {
+      if (!SK_CS_V3 && lane == 0) {
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         uint64_t* mb = &mbar[(t + 4) & 7];
         mb_expect_arrive(mb, two ? 2u * lbytes : lbytes);
@@ -2000,21 +2077,40 @@ __global__ void __launch_bounds__(kCsThreads, 1)
       cs_reduce_self<S>(Kb + (yl & (kCsKR - 1)) * KL + S, gseg + ((int64_t)yl * nstrip + sx) * NE, lane);
     } else {
       const int yl = y - 2;
+#ifdef SK_CS_DBG_SLOT0WAIT
+      if (rrole == 1) { const int j = t - 3 > 0 ? t - 3 : 0; mb_wait(&mbar[j & 7], (unsigned)(j >> 3) & 1u); }
+#endif
       cs_reduce_slot<S>(rrole == 1 ? Ar + (yl & (kCsAR - 1)) * AL + 2 * S : Kb + (yl & (kCsKR - 1)) * KL + S,
-                        Zs + (yl & 1) * ZL, gseg + ((int64_t)yl * nstrip + sx) * NE + NS + (rrole - 1) * NB, lane);
+                        Zs + (yl & (kCsZR - 1)) * ZL, gseg + ((int64_t)yl * nstrip + sx) * NE + NS + (rrole - 1) * NB, lane);
     }
     step_arrive(t);
   };
 #endif
   for (int y = ys; y <= y1 + 1; ++y) {
     const int t = y - ys;
+#ifdef SK_CS_DBG_V1LIKE
+#ifndef SK_CS_DBG_NOISSUERWAIT
+    if (issuer && lane == 0) mb_wait(&mbar[t & 7], (unsigned)(t >> 3) & 1u);
+#endif
+    __syncthreads();
+#endif
+#ifdef SK_CS_DBG_ISSUERWAIT
+    if (issuer && lane == 0) mb_wait(&mbar[t & 7], (unsigned)(t >> 3) & 1u);
+#endif
 #if SK_CS_FAST
     // reducers: y-2 >= y0, y-1 < y1, and the issued lines y+5, y+4 in [0, g)
-    if (warp > kCsColWarps && y >= y0 + 2 && y <= y1 - 1 && y + 5 < g && y + 4 >= 0 && y + 4 <= y1 + 1) {
-      red_step(y);
-      continue;
+    // reducers: one tight loop over all their interior steps (lines y-1 / y-2 inside the range;
+    // without V3 also the issued lines y+5, y+4 inside the grid and wanted: y <= min(y1-3, g-6))
+    if (warp > kCsColWarps && y == y0 + 2) {
+      const int ylast = SK_CS_V3 ? y1 - 1 : (y1 - 3 < g - 6 ? y1 - 3 : g - 6);
+      if (ylast >= y) {
+        for (; y <= ylast; ++y) red_step(y);
+        --y;
+        continue;
+      }
     }
-    if (warp <= kCsColWarps && y >= y0 + 1 && y + 2 <= y1 - 1) {
+    // (V3: the halo warp's lean issue needs lines y + 4 .. y + 6 inside the grid)
+    if (warp <= kCsColWarps && y >= y0 + 1 && y + 2 <= y1 - (SK_CS_V3 ? 2 : 1) && (!SK_CS_V3 || y + 6 < g)) {
       if (warp < kCsColWarps) {
         main_step(y);
         main_step(y + 1);
@@ -2031,6 +2127,15 @@ __global__ void __launch_bounds__(kCsThreads, 1)
     if (warp <= kCsColWarps) {
       const bool act = compute && y <= y1;
       double vq[kCsNC][S];
+#ifdef SK_CS_DBG_WAITTOP
+      if (t > 0) step_wait(t);
+#endif
+#ifdef SK_CS_DBG_NOPREF
+      if (act && t > 0) {  // operands loaded at the step of use (group t: lines y + 1 / y)
+        mb_wait(&mbar[t & 7], (unsigned)(t >> 3) & 1u);
+        load_a_ops(y);
+      }
+#endif
       if (act) {
         double* K0 = Kb + (y & (kCsKR - 1)) * KL;
         const bool wr = inner && y >= y0 && y < y1;
@@ -2074,10 +2179,17 @@ __global__ void __launch_bounds__(kCsThreads, 1)
             for (int u = 0; u < S; ++u) vq[q][u] = v[u];
           }
       }
+#ifndef SK_CS_DBG_WAITTOP
       if (t > 0) step_wait(t);
+#endif
+#if SK_CS_V3
+      // group t + 3: U_{k-1} line y + 4, U_{k-2} line y + 3 (the slots' last readers, the
+      // reducers of step t - 2 included, are done)
+      if (issuer && y + 3 <= y1 + 1) issue(t + 3, y + 4, y + 4, y + 3);
+#endif
       if (act) {
         const double* K1 = Kb + ((y - 1) & (kCsKR - 1)) * KL;
-        double* Z1 = Zs + ((y - 1) & 1) * ZL;
+        double* Z1 = Zs + ((y - 1) & (kCsZR - 1)) * ZL;
         const bool zl = inner && y - 1 >= y0 && y - 1 < y1;
         double kle[kCsNC][S], kri[kCsNC][S];
 #pragma unroll
@@ -2087,10 +2199,12 @@ __global__ void __launch_bounds__(kCsThreads, 1)
             sw_get<S>(K1 + ki - S, kle[q]);
             sw_get<S>(K1 + ki + S, kri[q]);
           }
+#ifndef SK_CS_DBG_NOPREF
         if (y + 1 <= y1) {
           mb_wait(&mbar[(t + 1) & 7], (unsigned)((t + 1) >> 3) & 1u);  // lines y + 2 (U_{k-1}), y + 1 (U_{k-2})
           load_a_ops(y + 1);
         }
+#endif
 #pragma unroll
         for (int q = 0; q < kCsNC; ++q)
           if (q < nslot) {
@@ -2112,7 +2226,9 @@ __global__ void __launch_bounds__(kCsThreads, 1)
       if (t > 0) step_wait(t);
       // group t + 4: U_{k-1} line y + 5, U_{k-2} line y + 4 (consumed from step t + 3 on; the
       // slots' last readers finished step t - 1)
+#if !SK_CS_V3
       if (issuer && y + 4 <= y1 + 1) issue(t + 4, y + 5, y + 5, y + 4);
+#endif
       const int r = warp - kCsColWarps - 1;
 #if SK_CS_NOINLINE_RED
       if (r == 0) {
@@ -2121,9 +2237,12 @@ __global__ void __launch_bounds__(kCsThreads, 1)
           cs_reduce_self<S>(Kb + (yl & (kCsKR - 1)) * KL + S, gseg + ((int64_t)yl * nstrip + sx) * NE, lane);
       } else {
         const int yl = y - 2;
+#ifdef SK_CS_DBG_SLOT0WAIT
+        if (r == 1 && yl >= y0 && yl < y1) { const int j = t - 3 > 0 ? t - 3 : 0; mb_wait(&mbar[j & 7], (unsigned)(j >> 3) & 1u); }
+#endif
         if (yl >= y0 && yl < y1)
           cs_reduce_slot<S>(r == 1 ? Ar + (yl & (kCsAR - 1)) * AL + 2 * S : Kb + (yl & (kCsKR - 1)) * KL + S,
-                            Zs + (yl & 1) * ZL, gseg + ((int64_t)yl * nstrip + sx) * NE + NS + (r - 1) * NB, lane);
+                            Zs + (yl & (kCsZR - 1)) * ZL, gseg + ((int64_t)yl * nstrip + sx) * NE + NS + (r - 1) * NB, lane);
       }
 #else
       if (r == 0) {
@@ -2156,7 +2275,7 @@ __global__ void __launch_bounds__(kCsThreads, 1)
         const int yl = y - 2;
         if (yl >= y0 && yl < y1) {
           const double* src = r == 1 ? Ar + (yl & (kCsAR - 1)) * AL + 2 * S : Kb + (yl & (kCsKR - 1)) * KL + S;
-          const double* Z = Zs + (yl & 1) * ZL;
+          const double* Z = Zs + (yl & (kCsZR - 1)) * ZL;
           double acc[NB];
 #pragma unroll
           for (int e = 0; e < NB; ++e) acc[e] = 0.0;
@@ -2181,6 +2300,9 @@ __global__ void __launch_bounds__(kCsThreads, 1)
 #endif
     }
     step_arrive(t);
+#ifdef SK_CS_DBG_SYNC
+    __syncthreads();
+#endif
   }
 #else
 #ifdef SK_CS_PROF2
@@ -2218,7 +2340,7 @@ __global__ void __launch_bounds__(kCsThreads, 1)
         const double* K1 = Kb + ((y - 1) & (kCsKR - 1)) * KL;
         const double* K2 = Kb + ((y - 2) & (kCsKR - 1)) * KL;
         (void)K2;
-        double* Z1 = Zs + ((y - 1) & 1) * ZL;
+        double* Z1 = Zs + ((y - 1) & (kCsZR - 1)) * ZL;
         const bool zl = inner && y - 1 >= y0 && y - 1 < y1;
         const bool wr = inner && y >= y0 && y < y1;
 #pragma unroll
@@ -2335,7 +2457,7 @@ __global__ void __launch_bounds__(kCsThreads, 1)
       } else if (y - 2 >= y0 && y - 2 < y1) {
         const int yl = y - 2;
         cs_reduce_slot<S>(r == 1 ? Ar + (yl & (kCsAR - 1)) * AL + 2 * S : Kb + (yl & (kCsKR - 1)) * KL + S,
-                          Zs + (yl & 1) * ZL, gseg + ((int64_t)yl * nstrip + sx) * NE + NS + (r - 1) * NB, lane);
+                          Zs + (yl & (kCsZR - 1)) * ZL, gseg + ((int64_t)yl * nstrip + sx) * NE + NS + (r - 1) * NB, lane);
       }
       if (true) {  // (the inline loops below are the SK_CS_NOINLINE_RED=0 variant)
       } else if (r == 0) {
@@ -2372,7 +2494,7 @@ __global__ void __launch_bounds__(kCsThreads, 1)
         if (yl >= y0 && yl < y1) {
           // slot 0: U_{k-1}(yl) . z'(yl); slot 1: U_k(yl) . z'(yl)
           const double* src = r == 1 ? Ar + (yl & (kCsAR - 1)) * AL + 2 * S : Kb + (yl & (kCsKR - 1)) * KL + S;
-          const double* Z = Zs + (yl & 1) * ZL;
+          const double* Z = Zs + (yl & (kCsZR - 1)) * ZL;
           double acc[NB];
 #pragma unroll
           for (int e = 0; e < NB; ++e) acc[e] = 0.0;
@@ -3741,7 +3863,7 @@ struct Launch {
     if constexpr (S <= 2) {
       const SideConst& sc = c.side[side0];
       const int nr = cols_ranges(sc, nz);
-      const size_t smem = sizeof(double) * ((kCsAR * kCsA + kCsBR * (SK_CS_TMA ? kCsA : kCsK) + kCsKR * kCsK + 2 * kSeg) * S);
+      const size_t smem = sizeof(double) * ((kCsAR * kCsA + kCsBR * (SK_CS_TMA ? kCsA : kCsK) + kCsKR * kCsK + kCsZR * kSeg) * S);
       static bool attr = false;
       if (!attr) {
         cudaFuncSetAttribute(k_lanczos_cols<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
