@@ -370,7 +370,13 @@ def main():
                           + ("larger than the 126 MB L2 (no flush needed)"
                              if 8 * cfg.a.n_rows * int(cfg.c1.shape[1]) > 126e6
                              else "L2-resident between passes (small config)")),
-                   "wall_s_timed_region": wall},
+                   "wall_s_timed_region": wall,
+                   "time_to_1e-8": (None if status == "converged" else
+                                    "unreachable within max_iter" + (
+                                        ": config 5 needs ~15,000 iterations = ~8 TB of basis (SURVEY App. A); one "
+                                        f"B200 holds ~{int(0.9 * 180e9 / (2 * 8 * cfg.a.n_rows * int(cfg.c1.shape[1]))) - 2} "
+                                        "iterations of both bases, so the fixed 200-iteration run and the residual it "
+                                        "reaches are what is reported" if args.config == 5 else ""))},
         "roofline": {"bound": dom_rf["bound"], "kernel": dom[0], "achieved": dom_rf["achieved"],
                      "peak": dom_rf["peak"],
                      "peak_source": peak_src if dom_rf["bound"] == "hbm" else fp64_peak["source"],
@@ -380,6 +386,7 @@ def main():
                      "classes": cls_out},
         "clocks": clocks,
         "gpu_launches": launches,
+        "time_to_tolerance_s": (dev_max / args.steps if status == "converged" else None),
     }
 
     if partitioned and not args.no_e2e:

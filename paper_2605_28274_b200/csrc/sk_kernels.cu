@@ -762,6 +762,82 @@ struct GramRing {
   static constexpr int STRIDE = 2 * (UNITS | 1);  // doubles
   static constexpr size_t BYTES = ON ? sizeof(double) * (size_t)8 * kGramStages * 32 * STRIDE : 0;
 };
+#ifndef SK_GRAM_NOINLINE
+#define SK_GRAM_NOINLINE 1
+#endif
+// One R1 segment of the Arnoldi Gram (rows base + lane + 32 m, m = 0 .. 15, of U_b against x,
+// output half h) as a separately compiled function: inside k_gram ptxas sank the loads of every
+// row to their first use (one row in flight per warp, long-scoreboard bound at 0.38 of HBM);
+// here rows are register double-buffered explicitly, two ahead of the accumulation. Returns the
+// lane's owner values of the xor butterflies (entry e lives in lane e & 31).
+template <int S>
+__device__ __noinline__ OwnerVals<(S / GramSplit<S>::H) * S> gram_segment(const double* __restrict__ ub,
+                                                                        const double* __restrict__ x, int64_t base,
+                                                                        int64_t n, int h, int lane) {
+  constexpr int H = GramSplit<S>::H, SU = S / H, NH = SU * S;
+  double acc[NH];
+#pragma unroll
+  for (int e = 0; e < NH; ++e) acc[e] = 0.0;
+  auto load = [&](int m, double* a, double* y) {
+    const int64_t i = base + lane + 32 * m;
+    if (i < n) {
+      ld_raw<S>(ub, i, a);
+      if constexpr (H == 1) {
+        ld_raw<S>(x, i, y);
+      } else {
+        const double2* py = reinterpret_cast<const double2*>(x + i * S + h * SU);
+#pragma unroll
+        for (int u = 0; u < SU / 2; ++u) {
+          const double2 v = __ldg(py + u);
+          y[2 * u] = v.x;
+          y[2 * u + 1] = v.y;
+        }
+      }
+    } else {
+#pragma unroll
+      for (int t = 0; t < S; ++t) a[t] = 0.0;
+#pragma unroll
+      for (int u = 0; u < SU; ++u) y[u] = 0.0;
+    }
+  };
+  // rows past n contribute acc + 0 * 0 = acc + (+0): the sums are unchanged bit for bit
+  // (acc starts at +0 and a + (+0) = a for every a, including -0 + (+0) = +0 = the skipped form
+  // only if acc were -0, which a sum starting at +0 with round-to-nearest never is)
+  double a0[S], y0[SU], a1[S], y1[SU];
+  load(0, a0, y0);
+  load(1, a1, y1);
+#pragma unroll
+  for (int m = 0; m < kLRows; m += 2) {
+    double a2[S], y2[SU], a3[S], y3[SU];
+    if (m + 2 < kLRows) {
+      load(m + 2, a2, y2);
+      load(m + 3, a3, y3);
+    }
+#pragma unroll
+    for (int u = 0; u < SU; ++u)
+#pragma unroll
+      for (int t = 0; t < S; ++t) acc[u * S + t] = __dadd_rn(acc[u * S + t], __dmul_rn(a0[t], y0[u]));
+#pragma unroll
+    for (int u = 0; u < SU; ++u)
+#pragma unroll
+      for (int t = 0; t < S; ++t) acc[u * S + t] = __dadd_rn(acc[u * S + t], __dmul_rn(a1[t], y1[u]));
+    if (m + 2 < kLRows) {
+#pragma unroll
+      for (int t = 0; t < S; ++t) {
+        a0[t] = a2[t];
+        a1[t] = a3[t];
+      }
+#pragma unroll
+      for (int u = 0; u < SU; ++u) {
+        y0[u] = y2[u];
+        y1[u] = y3[u];
+      }
+    }
+  }
+  OwnerVals<NH> out;
+  seg_butterfly<NH>(acc, out, lane);
+  return out;
+}
 template <int S>
 __global__ void __launch_bounds__(256, GramSplit<S>::MINB) k_gram(const __grid_constant__ SolveConst c, int mode) {
   constexpr int NB = S * S;
@@ -867,6 +943,12 @@ __global__ void __launch_bounds__(256, GramSplit<S>::MINB) k_gram(const __grid_c
     double acc[NH];
 #pragma unroll
     for (int e = 0; e < NH; ++e) acc[e] = 0.0;
+#if SK_GRAM_NOINLINE
+    if (q < g.nvalid_warp) {
+      segv[q] = gram_segment<S>(ub, x, (g.seg_w0 + q) * kSeg, n, h, lane);
+      continue;
+    }
+#endif
     if (q < g.nvalid_warp) {
       const int64_t base = (g.seg_w0 + q) * kSeg;
 #pragma unroll UNR

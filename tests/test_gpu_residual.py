@@ -120,3 +120,28 @@ def test_config5_true_residual_tracks_history(sk):
         sol.free()
     finally:
         prob.free()
+
+
+def test_fp64_peak_microbenchmark_is_sane(sk):
+    """sk_measure_fp64_peak (the FP64 roofline denominator in bench.py): DFMA chains reach
+    about twice the flop rate of mul-then-add chains, both in the B200's range."""
+    dfma, dmuladd = sk.measure_fp64_peak(0)
+    assert 15.0 < dfma < 90.0, dfma
+    assert 8.0 < dmuladd < 45.0, dmuladd
+    assert 1.5 < dfma / dmuladd < 2.5
+
+
+def test_copy_factors_staged_equals_blockwise(sk, po):
+    """sk_solution_copy_V/W (double-buffered export + multi-lane staged D2H) against the
+    column-range accessor."""
+    a = po.laplacian_2d(40)
+    c1, c2 = po.random_rhs(a.n_rows, 2, 3), po.random_rhs(a.n_rows, 2, 4)
+    sol = sk.factorized_cg(to_sk(sk, a), to_sk(sk, a), c1, c2, sk.SolverConfig(eps_tol=1e-6))
+    v = sol.V
+    ref = po.factorized_cg(a, a, c1, c2, po.Config(eps_tol=1e-6), po.REPRODUCIBLE)
+    assert np.array_equal(v, ref.V) and np.array_equal(sol.W, ref.W)
+    pv = sk.pinned_empty(v.shape)
+    import ctypes as C
+    from paper_2605_28274_b200 import _check, _p, lib
+    _check(lib().sk_solution_copy_V(sol._h, _p(pv)))
+    assert np.array_equal(pv, v)
