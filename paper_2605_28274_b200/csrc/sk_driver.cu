@@ -2001,6 +2001,7 @@ void tr_side_r(const TrSide& in, int wdt, double* R, cudaStream_t st, TrHandles&
   const double budget = std::min<double>((double)fr / 3.0, 8.0e9);
   const double per_row = 8.0 * (kb + (in.core ? r : 0) + r + wdt);
   int64_t rc = (int64_t)(budget / per_row) - 2 * halo;
+  if (wdt > 2048) rc = std::min<int64_t>(rc, (int64_t(1) << 27) / wdt - wdt);  // wide panels: see sk_solution_stacked_r
   rc = std::max<int64_t>(rc, 256);
   if (const char* e = getenv("SK_TR_CHUNK")) rc = std::max<int64_t>(1, std::atoll(e));  // tests: force several chunks
   rc = std::min<int64_t>(rc, n);
@@ -2254,6 +2255,9 @@ sk_status sk_solution_stacked_r(const sk_solution* sol, int32_t side, const doub
     CK(cudaMemGetInfo(&fr, &tot));
     const double budget = std::min<double>((double)fr / 3.0, 8.0e9);
     int64_t rc = (int64_t)(budget / (8.0 * (kb + 2.0 * wdt)));
+    // keep [R; chunk] under 2^27 elements: cuSOLVER geqrf faulted (illegal memory access) on a
+    // 74,591 x 5,816 panel at config 3 and runs clean at 22,200 x 5,816 (profiles/r2/xdist_debug.py)
+    rc = std::min<int64_t>(rc, (int64_t(1) << 27) / wdt - wdt);
     rc = std::max<int64_t>(rc, 256);
     if (const char* e = getenv("SK_TR_CHUNK")) rc = std::max<int64_t>(1, std::atoll(e));
     rc = std::min<int64_t>(rc, n);

@@ -1519,7 +1519,10 @@ __global__ void __launch_bounds__(kFusedThreads, kWaveBlocks)
 #endif
 constexpr int kCsNC = SK_CS_NC;            // grid columns per column thread
 constexpr int kCsColWarps = 16 / kCsNC;    // 512 columns
-constexpr int kCsRedWarps = 3;             // self-Gram, raw Gram slot 0, slot 1
+#ifndef SK_CS_RED5
+#define SK_CS_RED5 0  // (measured 1507 vs 1776 iter/s at C5: off) five reducer warps: self-Gram + (slot 0, slot 1) x (z' column u = 0, 1); needs SK_CS_V2 == 0
+#endif
+constexpr int kCsRedWarps = (SK_CS_RED5 && !SK_CS_V2) ? 5 : 3;  // self-Gram, raw Gram slots 0 / 1 (per z' column with RED5)
 constexpr int kCsThreads = 32 * (kCsColWarps + 1 + kCsRedWarps);
 constexpr int kCsA = kSeg + 4;             // U_{k-1} lines: columns x0-2 .. x0+513
 constexpr int kCsK = kSeg + 2;             // U_k / U_{k-2} lines: columns x0-1 .. x0+512
@@ -1714,6 +1717,44 @@ __device__ __noinline__ void cs_reduce_slot(const double* __restrict__ src, cons
     for (int e = 0; e < NB; ++e) {
       const double r = butterfly(acc[e]);
       if (lane == e) out[e] = r;
+    }
+  }
+}
+
+// One z' column of a raw-Gram slot: entries (u, t) = sum_rows src[row][t] * z'[row][u], t < S, for a
+// fixed u (RED5: the four entries of a slot at s = 2 are split over two warps, so no reducer warp
+// carries more than three entries per line). Same R1 order per entry as cs_reduce_slot.
+template <int S>
+__device__ __noinline__ void cs_reduce_slot_u(const double* __restrict__ src, const double* __restrict__ Z, int u,
+                                              double* __restrict__ out, int lane) {
+  double av[kLRows][S], zu[kLRows];
+#pragma unroll
+  for (int m = 0; m < kLRows; ++m) {
+    sw_get<S>(src + (lane + 32 * m) * S, av[m]);
+    zu[m] = Z[(lane + 32 * m) * S + u];
+  }
+  double acc[S];
+#pragma unroll
+  for (int t = 0; t < S; ++t) acc[t] = 0.0;
+#pragma unroll
+  for (int m = 0; m < kLRows; ++m)
+#pragma unroll
+    for (int t = 0; t < S; ++t) acc[t] = __dadd_rn(acc[t], __dmul_rn(av[m][t], zu[m]));
+  if constexpr (S == 2) {
+    // two butterflies with one halving exchange (see butterfly4): lanes with bit 4 clear end with
+    // entry t = 0, the others with t = 1
+    const bool h4 = (lane & 16) != 0;
+    double kk = h4 ? acc[1] : acc[0];
+    const double ss = h4 ? acc[0] : acc[1];
+    kk = __dadd_rn(kk, shfl_xor_d(ss, 16));
+#pragma unroll
+    for (int d = 8; d >= 1; d >>= 1) kk = __dadd_rn(kk, shfl_xor_d(kk, d));
+    if ((lane & 15) == 0) out[lane >> 4] = kk;
+  } else {
+#pragma unroll
+    for (int t = 0; t < S; ++t) {
+      const double r = butterfly(acc[t]);
+      if (lane == t) out[t] = r;
     }
   }
 }
@@ -2538,8 +2579,17 @@ __global__ void __launch_bounds__(kCsThreads, 1)
           cs_reduce_self<S>(Kb + (yl & (kCsKR - 1)) * KL + S, gseg + ((int64_t)yl * nstrip + sx) * NE, lane);
       } else if (y - 2 >= y0 && y - 2 < y1) {
         const int yl = y - 2;
-        cs_reduce_slot<S>(r == 1 ? Ar + (yl & (kCsAR - 1)) * AL + 2 * S : Kb + (yl & (kCsKR - 1)) * KL + S,
-                          Zs + (yl & (kCsZR - 1)) * ZL, gseg + ((int64_t)yl * nstrip + sx) * NE + NS + (r - 1) * NB, lane);
+        if constexpr (kCsRedWarps == 5) {
+          const int slot = (r - 1) >> 1, u = (r - 1) & 1;  // warps 1, 2: slot 0 (U_{k-1}); 3, 4: slot 1 (U_k)
+          if (u < S)
+            cs_reduce_slot_u<S>(slot == 0 ? Ar + (yl & (kCsAR - 1)) * AL + 2 * S : Kb + (yl & (kCsKR - 1)) * KL + S,
+                                Zs + (yl & (kCsZR - 1)) * ZL, u,
+                                gseg + ((int64_t)yl * nstrip + sx) * NE + NS + slot * NB + u * S, lane);
+        } else {
+          cs_reduce_slot<S>(r == 1 ? Ar + (yl & (kCsAR - 1)) * AL + 2 * S : Kb + (yl & (kCsKR - 1)) * KL + S,
+                            Zs + (yl & (kCsZR - 1)) * ZL, gseg + ((int64_t)yl * nstrip + sx) * NE + NS + (r - 1) * NB,
+                            lane);
+        }
       }
       if (true) {  // (the inline loops below are the SK_CS_NOINLINE_RED=0 variant)
       } else if (r == 0) {
