@@ -430,11 +430,11 @@ def main():
                 if factors:                          # FactorizedSolution returns V, W by value
                     v = sol.V                        # (factorized_solvers.cpp:194-195)
                     nb += v.nbytes
+                    del v                            # one factor at a time on the host (54 GB each at C5)
                     if cfg.method != "cg_lyapunov":
                         w = sol.W
                         nb += w.nbytes
                         del w
-                    del v
                 dt = time.perf_counter() - t0
                 if it > 0:
                     e_s += dt
@@ -458,7 +458,17 @@ def main():
         if c2h is not c1h:
             c2h[...] = cfg.c2
         line["e2e_pinned_inputs"] = e2e_leg(c1h, c2h, args.e2e_steps)
-        if not args.no_factors:
+        need = 8.0 * (cfg.a.n_rows + (0 if cfg.b is None else cfg.b.n_rows)) * (iters // max(args.steps, 1) + 2) * int(cfg.c1.shape[1])
+        avail = None
+        try:
+            for ln in open("/proc/meminfo"):
+                if ln.startswith("MemAvailable"):
+                    avail = 1024.0 * float(ln.split()[1])
+        except OSError:
+            pass
+        if not args.no_factors and avail is not None and avail < 0.8 * need:
+            line["e2e_with_factors"] = {"value": None, "unit": UNIT, "note": f"skipped: V and W need {need / 1e9:.0f} GB of host memory, {avail / 1e9:.0f} GB available"}
+        elif not args.no_factors:
             # the reference's by-value FactorizedSolution: V and W copied to host memory too
             line["e2e_with_factors"] = e2e_leg(cfg.c1, cfg.c2, 1, factors=True)
             line["e2e_with_factors"]["note"] = ("as e2e plus V and W normalised on the device and copied to pageable "
