@@ -431,10 +431,12 @@ def main():
                     v = sol.V                        # (factorized_solvers.cpp:194-195)
                     nb += v.nbytes
                     del v                            # one factor at a time on the host (54 GB each at C5)
+                    sol._V = None                    # (the mirror caches the copy: drop it)
                     if cfg.method != "cg_lyapunov":
                         w = sol.W
                         nb += w.nbytes
                         del w
+                        sol._W = None
                 dt = time.perf_counter() - t0
                 if it > 0:
                     e_s += dt
