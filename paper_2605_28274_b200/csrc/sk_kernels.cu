@@ -1976,6 +1976,9 @@ __global__ void __launch_bounds__(kCsThreads, 1)
   }
   __syncthreads();
   auto step_arrive = [&](int t) {
+#ifdef SK_CS_DBG_FENCE
+    __threadfence_block();  // every lane's shared-memory stores performed before lane 0's arrive
+#endif
     __syncwarp();
     if (lane == 0)
       asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(
