@@ -747,23 +747,33 @@ struct GramSplit {
   static constexpr int MINB = H == 2 ? 2 : (S <= 4 ? 3 : 1);  // CTAs per SM (register budget)
 };
 #ifndef SK_GRAM_RING
-#define SK_GRAM_RING 0  // cp.async row ring: measured slower at config 4 (20.2 s vs 17.0 s), kept for reference
+#define SK_GRAM_RING 0  // cp.async row rings, per-lane rows (20.2 s at config 4) and coalesced pieces (17.4 s), against 17.0 s: LDGSTS costs the L1TEX pipe on both sides
 #endif
 #ifndef SK_GRAM_STAGES
 #define SK_GRAM_STAGES 3
 #endif
 constexpr int kGramStages = SK_GRAM_STAGES;
-// shared-memory row ring of k_gram (even S: 16-byte aligned rows): per lane S doubles of
-// U_b and S / H of x, padded to an odd number of 16-byte units
+// Shared-memory row ring of k_gram (even S: rows are whole 16-byte units). ncu (profiles/r2):
+// k_gram<8> ran with the L1TEX pipe 92% busy and DRAM 30%, L2 31%, FP64 29% -- a lane reading
+// its own 64-byte row makes every LDG.128 of the warp touch 16 cache lines for 512 useful bytes.
+// Here the warp copies the 32 consecutive rows of a step as CONTIGUOUS 16-byte pieces (cp.async,
+// lane l takes pieces l, l + 32, ...: four fully used lines per instruction) into a per-warp
+// ring whose rows are padded to an odd number of 16-byte units, so the lane's own row then
+// comes out of shared memory conflict-free.
 template <int S>
 struct GramRing {
   static constexpr bool ON = (S % 2 == 0);
-  static constexpr int UNITS = (S + S / GramSplit<S>::H) / 2;
-  static constexpr int STRIDE = 2 * (UNITS | 1);  // doubles
-  static constexpr size_t BYTES = ON ? sizeof(double) * (size_t)8 * kGramStages * 32 * STRIDE : 0;
+  static constexpr int SU = S / GramSplit<S>::H;
+  static constexpr int UA = S / 2, UY = SU / 2;      // 16-byte units per row of U_b / of x's half
+  static constexpr int PA = UA | 1, PY = UY | 1;     // padded row strides (units)
+  static constexpr int STAGE = 32 * (PA + PY) * 2;   // doubles per warp and stage
+  static constexpr size_t BYTES = ON ? sizeof(double) * (size_t)8 * kGramStages * STAGE : 0;
 };
 #ifndef SK_GRAM_NOINLINE
 #define SK_GRAM_NOINLINE 1
+#endif
+#ifndef SK_GRAM_XPOSE
+#define SK_GRAM_XPOSE 1  // s = 4, 8: coalesced loads with transposed accumulator ownership
 #endif
 // One R1 segment of the Arnoldi Gram (rows base + lane + 32 m, m = 0 .. 15, of U_b against x,
 // output half h) as a separately compiled function: inside k_gram ptxas sank the loads of every
@@ -867,28 +877,32 @@ __global__ void __launch_bounds__(256, GramSplit<S>::MINB) k_gram(const __grid_c
   OwnerVals<NH> segv[kSegsPerWarp];
 #if SK_GRAM_RING
   if constexpr (GramRing<S>::ON) {
-    // Rows reach the registers through a per-warp shared-memory ring filled by cp.async
-    // kGramStages - 1 row steps ahead (a lane copies its own row of U_b and of x and reads
-    // back only what it copied: no barrier; the lane stride is an odd number of 16-byte
-    // units, so both directions are conflict-free). The loads of step t + D - 1 are in
-    // flight while step t is accumulated; the per-lane order m = 0..15 of R1 is unchanged.
-    constexpr int D = kGramStages, ST = GramRing<S>::STRIDE;
+    using GR = GramRing<S>;
+    constexpr int D = kGramStages, UA = GR::UA, UY = GR::UY, PA = GR::PA, PY = GR::PY;
     extern __shared__ __align__(16) double gram_ring[];
-    double* my = gram_ring + ((size_t)(threadIdx.x >> 5) * D * 32 + lane) * ST;
+    double* wring = gram_ring + (size_t)(threadIdx.x >> 5) * D * GR::STAGE;
     const int nsteps = g.nvalid_warp * kLRows;
     auto issue = [&](int step) {
       if (step < nsteps) {
-        const int64_t i = (g.seg_w0 + step / kLRows) * kSeg + lane + 32 * (step % kLRows);
-        if (i < n) {
-          const unsigned d = (unsigned)__cvta_generic_to_shared(my + (size_t)(step % D) * 32 * ST);
-          const double* ga = ub + i * S;
-          const double* gy = x + i * S + h * SU;
+        const int64_t row0 = (g.seg_w0 + step / kLRows) * kSeg + 32 * (step % kLRows);
+        double* sa = wring + (size_t)(step % D) * GR::STAGE;
+        double* sy = sa + 32 * PA * 2;
 #pragma unroll
-          for (int t = 0; t < S / 2; ++t)
-            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d + 16 * t), "l"(ga + 2 * t) : "memory");
+        for (int j = 0; j < UA; ++j) {
+          const int p_ = lane + 32 * j, rr = p_ / UA, cc = p_ % UA;
+          if (row0 + rr < n)
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
+                             (unsigned)__cvta_generic_to_shared(sa + (rr * PA + cc) * 2)),
+                         "l"(ub + (row0 + rr) * S + cc * 2)
+                         : "memory");
+        }
 #pragma unroll
-          for (int u = 0; u < SU / 2; ++u)
-            asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(d + 8 * S + 16 * u), "l"(gy + 2 * u)
+        for (int j = 0; j < UY; ++j) {
+          const int p_ = lane + 32 * j, rr = p_ / UY, cc = p_ % UY;
+          if (row0 + rr < n)
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(
+                             (unsigned)__cvta_generic_to_shared(sy + (rr * PY + cc) * 2)),
+                         "l"(x + (row0 + rr) * S + h * SU + cc * 2)
                          : "memory");
         }
       }
@@ -906,21 +920,25 @@ __global__ void __launch_bounds__(256, GramSplit<S>::MINB) k_gram(const __grid_c
 #pragma unroll 2
         for (int m = 0; m < kLRows; ++m) {
           const int step = q * kLRows + m;
+          // this step's pieces (copied by all lanes) have landed, and every lane is done
+          // reading the stage the next issue overwrites
+          asm volatile("cp.async.wait_group %0;" ::"n"(D - 2) : "memory");
+          __syncwarp();
           issue(step + D - 1);
-          asm volatile("cp.async.wait_group %0;" ::"n"(D - 1) : "memory");
           const int64_t i = base + lane + 32 * m;
           if (i < n) {
-            const double* sp = my + (size_t)(step % D) * 32 * ST;
+            const double* sa = wring + (size_t)(step % D) * GR::STAGE + lane * PA * 2;
+            const double* sy = wring + (size_t)(step % D) * GR::STAGE + 32 * PA * 2 + lane * PY * 2;
             double a[S], y[SU];
 #pragma unroll
-            for (int t = 0; t < S / 2; ++t) {
-              const double2 v = reinterpret_cast<const double2*>(sp)[t];
+            for (int t = 0; t < UA; ++t) {
+              const double2 v = reinterpret_cast<const double2*>(sa)[t];
               a[2 * t] = v.x;
               a[2 * t + 1] = v.y;
             }
 #pragma unroll
-            for (int u = 0; u < SU / 2; ++u) {
-              const double2 v = reinterpret_cast<const double2*>(sp + S)[u];
+            for (int u = 0; u < UY; ++u) {
+              const double2 v = reinterpret_cast<const double2*>(sy)[u];
               y[2 * u] = v.x;
               y[2 * u + 1] = v.y;
             }
@@ -943,6 +961,88 @@ __global__ void __launch_bounds__(256, GramSplit<S>::MINB) k_gram(const __grid_c
     double acc[NH];
 #pragma unroll
     for (int e = 0; e < NH; ++e) acc[e] = 0.0;
+#if SK_GRAM_XPOSE
+    if constexpr (S == 8 || S == 4) {
+      // Transposed ownership (ncu, profiles/r2: the L1TEX pipe was 92% busy because a lane
+      // reading its own row makes every LDG.128 touch 16 lines): the warp loads the step's 32
+      // consecutive rows as contiguous 16-byte pieces, so lane p holds column pair c = p % UA of
+      // the rows rho = p / UA + RP j (j < UA) and accumulates, for those UA logical lanes, the
+      // entries (u, 2c), (u, 2c + 1). Every logical lane's sum still runs over the steps
+      // m = 0 .. 15 in order; the xor butterfly over logical lanes (d = 16 .. 1) has its high
+      // rounds inside the thread (IEEE addition is commutative: both partners hold the same
+      // bits) and its low rounds as shuffles by d UA. Bitwise the row-per-lane form.
+      constexpr int UA = S / 2, RP = 32 / UA;
+      const int cpair = lane % UA, rho0 = lane / UA;
+      double acc2[UA][SU][2];
+#pragma unroll
+      for (int j = 0; j < UA; ++j)
+#pragma unroll
+        for (int u = 0; u < SU; ++u) acc2[j][u][0] = acc2[j][u][1] = 0.0;
+      if (q < g.nvalid_warp) {
+        const int64_t base = (g.seg_w0 + q) * kSeg;
+#pragma unroll 2
+        for (int m = 0; m < kLRows; ++m) {
+          const int64_t r0 = base + 32 * m;
+          double2 av[UA];
+          double yv[UA][SU];
+#pragma unroll
+          for (int j = 0; j < UA; ++j) {
+            const int64_t i = r0 + rho0 + RP * j;
+            if (i < n) {
+              av[j] = __ldg(reinterpret_cast<const double2*>(ub + i * S) + cpair);
+              const double2* py = reinterpret_cast<const double2*>(x + i * S + h * SU);
+#pragma unroll
+              for (int u = 0; u < SU / 2; ++u) {
+                const double2 v = __ldg(py + u);
+                yv[j][2 * u] = v.x;
+                yv[j][2 * u + 1] = v.y;
+              }
+            } else {
+              av[j] = make_double2(0.0, 0.0);
+#pragma unroll
+              for (int u = 0; u < SU; ++u) yv[j][u] = 0.0;
+            }
+          }
+#pragma unroll
+          for (int j = 0; j < UA; ++j)
+#pragma unroll
+            for (int u = 0; u < SU; ++u) {
+              acc2[j][u][0] = __dadd_rn(acc2[j][u][0], __dmul_rn(av[j].x, yv[j][u]));
+              acc2[j][u][1] = __dadd_rn(acc2[j][u][1], __dmul_rn(av[j].y, yv[j][u]));
+            }
+        }
+      }
+      // butterfly over the logical lanes: in-thread rounds (lane bits held by j), then shuffles
+      double ent[SU][2];
+#pragma unroll
+      for (int u = 0; u < SU; ++u)
+#pragma unroll
+        for (int b2 = 0; b2 < 2; ++b2) {
+          double w_[UA];
+#pragma unroll
+          for (int j = 0; j < UA; ++j) w_[j] = acc2[j][u][b2];
+#pragma unroll
+          for (int dj = UA / 2; dj >= 1; dj >>= 1)
+#pragma unroll
+            for (int j = 0; j < dj; ++j) w_[j] = __dadd_rn(w_[j], w_[j + dj]);
+          double v = w_[0];
+#pragma unroll
+          for (int d = RP / 2; d >= 1; d >>= 1) v = __dadd_rn(v, shfl_xor_d(v, d * UA));
+          ent[u][b2] = v;
+        }
+      // entry e = u S + t of this half lives in the lanes with p % UA == t / 2: hand it to lane e
+      double mine = 0.0;
+#pragma unroll
+      for (int u = 0; u < SU; ++u)
+#pragma unroll
+        for (int b2 = 0; b2 < 2; ++b2) {
+          const double got = __shfl_sync(0xffffffffu, ent[u][b2], (lane % S) >> 1);
+          if (lane / S == u && (lane & 1) == b2) mine = got;
+        }
+      segv[q].v[0] = mine;
+      continue;
+    }
+#endif
 #if SK_GRAM_NOINLINE
     if (q < g.nvalid_warp) {
       segv[q] = gram_segment<S>(ub, x, (g.seg_w0 + q) * kSeg, n, h, lane);
