@@ -1310,9 +1310,7 @@ struct Solver {
         timed(3, pass_bytes(k, 2), [&] { sk::launch_lanczos_update(c, k + 1, st); });
         dbg("update", k);
       }
-      if (pause_mode) {
-        sk::launch_dist_pause(c, st);
-      } else {
+      if (!pause_mode) {  // (pause mode: k_cg_a checks the stages itself and publishes PAUSED)
         timed(2, 0.0, [&] { sk::launch_rare(c, k + 1, st); });
       }
       dbg("rare", k);

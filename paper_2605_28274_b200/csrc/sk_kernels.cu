@@ -3664,6 +3664,21 @@ template <int S>
 __global__ void __launch_bounds__(256) k_cg_a(const __grid_constant__ SolveConst c) {
   DevState* st = c.st;
   if (st->status != RUNNING) return;
+  // pause check (was a kernel of its own, ~4 us per iteration): an extension that asked for a
+  // rare path (Householder / clean-up) stops the run here; every CTA takes the same decision
+  // from the stages the extension kernel left, one thread publishes it. The host sees PAUSED
+  // in the status ring, runs the rare kernels and resumes (sk_driver.cu).
+  {
+    bool need = false;
+    for (int sd = 0; sd < c.nsides; ++sd) {
+      const int g = st->side[sd].stage;
+      need = need || g == ST_NEED_HH || g == ST_NEED_CLEANUP;
+    }
+    if (need) {
+      if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) st->status = PAUSED;
+      return;
+    }
+  }
   if (any_side_broken(c)) {
     if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) {
       st->status = BREAKDOWN;
