@@ -2068,27 +2068,47 @@ __global__ void __launch_bounds__(kCsThreads, 1)
     if (producer && t >= 2) mb_wait(&rbar[(t - 2) & 3], (unsigned)((t - 2) >> 2) & 1u);
   };
 #else
-  __shared__ __align__(8) uint64_t sbar[2];
+#ifdef SK_CS_DBG_PADBAR
+  __shared__ __align__(128) uint64_t sbar_pad[48];  // step barriers 128 bytes apart and away from mbar[]
+  uint64_t* sbar = sbar_pad + 16;
+  constexpr int kSbStride = 16;
+#else
+  __shared__ __align__(8) uint64_t sbar_arr[2];
+  uint64_t* sbar = sbar_arr;
+  constexpr int kSbStride = 1;
+#endif
+#ifdef SK_CS_DBG_ALLARRIVE
+  constexpr unsigned kSbCount = kCsThreads;  // every thread arrives for itself
+#else
+  constexpr unsigned kSbCount = kCsThreads / 32;
+#endif
   if (threadIdx.x < 2) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"((unsigned)__cvta_generic_to_shared(&sbar[threadIdx.x])),
-                 "r"((unsigned)(kCsThreads / 32))
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(
+                     (unsigned)__cvta_generic_to_shared(&sbar[threadIdx.x * kSbStride])),
+                 "r"(kSbCount)
                  : "memory");
   }
   __syncthreads();
   auto step_arrive = [&](int t) {
+#ifdef SK_CS_DBG_ALLARRIVE
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(
+                     (unsigned)__cvta_generic_to_shared(&sbar[((t + 1) & 1) * kSbStride]))
+                 : "memory");
+#else
 #ifdef SK_CS_DBG_FENCE
     __threadfence_block();  // every lane's shared-memory stores performed before lane 0's arrive
 #endif
     __syncwarp();
     if (lane == 0)
       asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(
-                       (unsigned)__cvta_generic_to_shared(&sbar[(t + 1) & 1]))
+                       (unsigned)__cvta_generic_to_shared(&sbar[((t + 1) & 1) * kSbStride]))
                    : "memory");
+#endif
   };
   auto step_wait = [&](int t) {  // all warps finished step t - 1 (t >= 1)
 #ifndef SK_CS_DBG_V1LIKE
     const unsigned par = (t & 1) ? (unsigned)(t >> 1) & 1u : (unsigned)((t >> 1) + 1) & 1u;
-    mb_wait(&sbar[t & 1], par);
+    mb_wait(&sbar[(t & 1) * kSbStride], par);
 #endif
   };
 #endif

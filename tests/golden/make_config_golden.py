@@ -104,7 +104,12 @@ if __name__ == "__main__":
     ap.add_argument("--threads", type=int, default=len(os.sched_getaffinity(0)))
     ap.add_argument("--modes", default="reproducible,reference_order")
     ap.add_argument("--window", type=int, default=None, help="override the leading-iteration window")
+    ap.add_argument("--full", action="store_true", help="no window (config 4 needs ~60 GB of host memory per mode)")
+    ap.add_argument("--out-dir", default=None, help="write the JSON files here instead of tests/golden")
     args = ap.parse_args()
+    if args.out_dir:
+        HERE = args.out_dir
+        os.makedirs(HERE, exist_ok=True)
     for idx in args.configs:
         for mode_name in args.modes.split(","):
-            run(idx, mode_name, args.threads, args.window or WINDOWS.get(idx))
+            run(idx, mode_name, args.threads, None if args.full else (args.window or WINDOWS.get(idx)))
