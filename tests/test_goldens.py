@@ -1,0 +1,47 @@
+"""Schema and consistency of the cached oracle histories (tests/golden/config*_*.json) and of the
+two arithmetic modes against each other at the BASELINE configs (CPU only: no oracle run)."""
+import json
+import os
+
+import numpy as np
+import pytest
+
+GOLD = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+EXPECT = {1: ("converged", 236), 2: ("converged", 520), 3: ("converged", 2908), 4: ("converged", 197),
+          5: ("max_iter", 200)}
+
+
+def load(idx, mode):
+    return json.load(open(os.path.join(GOLD, f"config{idx}_{mode}.json")))
+
+
+@pytest.mark.parametrize("idx", [1, 2, 3, 4, 5])
+def test_reproducible_golden_is_a_full_run(idx):
+    g = load(idx, "reproducible")
+    assert g["window"] is None
+    assert (g["status"], g["iterations"]) == EXPECT[idx]
+    h = g["rel_residual"]
+    assert len(h) == g["iterations"] + 1 and h[0] == 1.0
+    if g["status"] == "converged":
+        assert h[-1] <= 1e-8 < h[-2]
+    assert g["paths"]["householder"] == 0 and g["paths"]["cleanup"] == 0
+
+
+@pytest.mark.parametrize("idx", [1, 3, 5])
+def test_cg_family_modes_agree_to_1e10_over_the_whole_run(idx):
+    """North-star bar for the CG family, oracle against oracle: the contract mode (which the
+    GPU executes bit for bit) vs the reference order, whole run, identical iteration counts."""
+    a, b = load(idx, "reproducible"), load(idx, "reference_order")
+    assert a["iterations"] == b["iterations"] and a["status"] == b["status"]
+    x, y = np.array(a["rel_residual"]), np.array(b["rel_residual"])
+    assert np.max(np.abs(x - y) / np.abs(y)) <= 1e-10
+
+
+@pytest.mark.parametrize("idx,window", [(2, 12), (4, 12)])
+def test_bicgstab_modes_agree_inside_the_window(idx, window):
+    a, b = load(idx, "reproducible"), load(idx, "reference_order")
+    x, y = np.array(a["rel_residual"][: window + 1]), np.array(b["rel_residual"][: window + 1])
+    assert np.max(np.abs(x - y) / np.abs(y)) <= 1e-10
+    if b["window"] is None:  # full reference-order run available: counts inside the sensitivity
+        assert a["status"] == b["status"] == "converged"
+        assert abs(a["iterations"] - b["iterations"]) <= 8
