@@ -57,6 +57,14 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "Krylov iters/sec (factorized CG; also time-to-tolerance and HBM GB/s vs peak)"
+# the GPU arm's config.workload strings (paper_2605_28274_b200/problems.py), repeated for the CPU arm
+WORKLOADS = {
+    1: "C1: factorized CG, 2D Laplacian 64x64 (n=m=4096), s=1, unit-norm columns",
+    2: "C2: factorized BiCGSTAB, 2D conv-diff 256^2, Pe 10, winds (1,1)/(1,-1), s=4",
+    3: "C3: factorized CG Lyapunov, 2D Laplacian 1024^2 (n=1,048,576), s=1",
+    4: "C4: factorized BiCGSTAB, 3D conv-diff 128^3 (Pe 5) x 3D Laplacian 64^3, s=8",
+    5: "C5: factorized CG, 2D Laplacian 4096^2 (n=m=16,777,216), s=2, 200 iterations",
+}
 UNIT = "iter/s"
 
 
@@ -245,7 +253,10 @@ def run_reference(args, rank, world):
         "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * secs / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic", "config": {"workload": f"C{args.config}", "sample": f"iterations 2..{iters + 1}"},
+        "data": "synthetic (seeded random_rhs N(0,1) blocks, stencil operators; BASELINE.json configs)",
+        "config": {"workload": WORKLOADS.get(args.config, f"C{args.config}"), "n": int(cpu_inputs(args.config)[1].n_rows),
+                   "s": int(cpu_inputs(args.config)[3].shape[1]), "sample": f"iterations 2..{iters + 1} of the workload "
+                   "(bounded CPU sample; the GPU arm runs the whole workload)", "parallelism": f"{threads} host threads"},
         "host": host_info(),
         "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -255,10 +266,11 @@ def run_reference(args, rank, world):
 
 def main():
     args = parse()
-    rank, world, local, dist = dist_setup(args)
     if args.impl == "reference":
-        run_reference(args, rank, world)
+        # CPU arm: rank 0 alone runs and prints; no process group, no GPU
+        run_reference(args, int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")))
         return
+    rank, world, local, dist = dist_setup(args)
     import numpy as np
     import paper_2605_28274_b200 as sk
     from paper_2605_28274_b200 import build as skbuild
