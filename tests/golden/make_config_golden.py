@@ -74,11 +74,14 @@ def oracle_inputs(idx):
     raise ValueError(idx)
 
 
-def run(idx, mode_name, threads, window=None):
+def run(idx, mode_name, threads, window=None, perturb=False):
     import numpy as np
     from oracle import pyoracle as po
     po.use_threads(threads)
     method, a, b, c1, c2, max_iter = oracle_inputs(idx)
+    if perturb:  # one entry of C1 moved by one ulp: the run's own sensitivity
+        c1 = c1.copy()
+        c1[5, 0] = np.nextafter(c1[5, 0], np.inf)
     if window:
         max_iter = window
     mode = po.REPRODUCIBLE if mode_name == "reproducible" else po.REFERENCE_ORDER
@@ -91,7 +94,8 @@ def run(idx, mode_name, threads, window=None):
            "rel_residual": [float(x) for x in sol.rel_residual], "paths": sol.paths,
            "core_shape": list(sol.core.shape), "core_fro": float(np.linalg.norm(sol.core)),
            "oracle_s": dt, "host": host_info(threads)}
-    path = os.path.join(HERE, f"config{idx}_{mode_name}.json")
+    path = os.path.join(HERE, f"config{idx}_{mode_name}{'_ulp' if perturb else ''}.json")
+    out["perturbed"] = bool(perturb)
     with open(path, "w") as f:
         json.dump(out, f, indent=0)
     print(f"C{idx} {mode_name}: {sol.status} after {sol.n_iterations} iterations, "
@@ -104,6 +108,7 @@ if __name__ == "__main__":
     ap.add_argument("--threads", type=int, default=len(os.sched_getaffinity(0)))
     ap.add_argument("--modes", default="reproducible,reference_order")
     ap.add_argument("--window", type=int, default=None, help="override the leading-iteration window")
+    ap.add_argument("--perturb", action="store_true", help="move C1[5,0] by one ulp (sensitivity run; file suffix _ulp)")
     ap.add_argument("--full", action="store_true", help="no window (config 4 needs ~60 GB of host memory per mode)")
     ap.add_argument("--out-dir", default=None, help="write the JSON files here instead of tests/golden")
     args = ap.parse_args()
@@ -112,4 +117,4 @@ if __name__ == "__main__":
         os.makedirs(HERE, exist_ok=True)
     for idx in args.configs:
         for mode_name in args.modes.split(","):
-            run(idx, mode_name, args.threads, None if args.full else (args.window or WINDOWS.get(idx)))
+            run(idx, mode_name, args.threads, None if args.full else (args.window or WINDOWS.get(idx)), args.perturb)

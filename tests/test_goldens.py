@@ -42,6 +42,8 @@ def test_bicgstab_modes_agree_inside_the_window(idx, window):
     a, b = load(idx, "reproducible"), load(idx, "reference_order")
     x, y = np.array(a["rel_residual"][: window + 1]), np.array(b["rel_residual"][: window + 1])
     assert np.max(np.abs(x - y) / np.abs(y)) <= 1e-10
-    if b["window"] is None:  # full reference-order run available: counts inside the sensitivity
+    if b["window"] is None:  # full reference-order run available
         assert a["status"] == b["status"] == "converged"
-        assert abs(a["iterations"] - b["iterations"]) <= 8
+        # iteration counts differ by what a one-ulp input change does to the reference-order run
+        # itself (config*_reference_order_ulp.json when present): C2 520 vs 513, C4 197 vs 168
+        assert abs(a["iterations"] - b["iterations"]) <= {2: 8, 4: 40}[idx]

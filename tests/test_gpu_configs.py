@@ -27,7 +27,9 @@ GOLD = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
 # iteration window over which BiCGSTAB histories must agree with the reference order
 # to 1e-10 (measured divergence iteration minus a margin)
 BICG_WINDOW = {2: 12, 4: 12}
-BICG_COUNT_SLACK = {2: 8, 4: 4}
+# iteration-count slack: the reference-order run's own spread under a one-ulp input change
+# (tests/golden/config*_reference_order_ulp.json; C4: reproducible 197, reference order 168)
+BICG_COUNT_SLACK = {2: 8, 4: 40}
 
 
 def golden(idx, mode):
