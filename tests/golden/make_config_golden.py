@@ -79,7 +79,9 @@ def run(idx, mode_name, threads, window=None, perturb=False):
     from oracle import pyoracle as po
     po.use_threads(threads)
     method, a, b, c1, c2, max_iter = oracle_inputs(idx)
-    if perturb:  # one entry of C1 moved by one ulp: the run's own sensitivity
+    if perturb == "all":  # every entry of C1 scaled by (1 + 2^-52): rounding-level change everywhere
+        c1 = c1 * (1.0 + 2.0 ** -52)
+    elif perturb:  # one entry of C1 moved by one ulp: the run's own sensitivity
         c1 = c1.copy()
         c1[5, 0] = np.nextafter(c1[5, 0], np.inf)
     if window:
@@ -94,7 +96,7 @@ def run(idx, mode_name, threads, window=None, perturb=False):
            "rel_residual": [float(x) for x in sol.rel_residual], "paths": sol.paths,
            "core_shape": list(sol.core.shape), "core_fro": float(np.linalg.norm(sol.core)),
            "oracle_s": dt, "host": host_info(threads)}
-    path = os.path.join(HERE, f"config{idx}_{mode_name}{'_ulp' if perturb else ''}.json")
+    path = os.path.join(HERE, f"config{idx}_{mode_name}{('_ulpall' if perturb == 'all' else '_ulp') if perturb else ''}.json")
     out["perturbed"] = bool(perturb)
     with open(path, "w") as f:
         json.dump(out, f, indent=0)
@@ -109,6 +111,7 @@ if __name__ == "__main__":
     ap.add_argument("--modes", default="reproducible,reference_order")
     ap.add_argument("--window", type=int, default=None, help="override the leading-iteration window")
     ap.add_argument("--perturb", action="store_true", help="move C1[5,0] by one ulp (sensitivity run; file suffix _ulp)")
+    ap.add_argument("--perturb-all", action="store_true", help="scale all of C1 by 1 + 2^-52 (file suffix _ulpall)")
     ap.add_argument("--full", action="store_true", help="no window (config 4 needs ~60 GB of host memory per mode)")
     ap.add_argument("--out-dir", default=None, help="write the JSON files here instead of tests/golden")
     args = ap.parse_args()
@@ -117,4 +120,4 @@ if __name__ == "__main__":
         os.makedirs(HERE, exist_ok=True)
     for idx in args.configs:
         for mode_name in args.modes.split(","):
-            run(idx, mode_name, args.threads, None if args.full else (args.window or WINDOWS.get(idx)), args.perturb)
+            run(idx, mode_name, args.threads, None if args.full else (args.window or WINDOWS.get(idx)), 'all' if args.perturb_all else args.perturb)

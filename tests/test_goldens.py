@@ -47,3 +47,23 @@ def test_bicgstab_modes_agree_inside_the_window(idx, window):
         # iteration counts differ by what a one-ulp input change does to the reference-order run
         # itself (config*_reference_order_ulp.json when present): C2 520 vs 513, C4 197 vs 168
         assert abs(a["iterations"] - b["iterations"]) <= {2: 8, 4: 40}[idx]
+
+
+def test_config2_reference_order_moves_more_under_one_ulp_than_the_contract_mode_differs():
+    """BASELINE config 2 at full size: the reference-order run against ITSELF with one entry of
+    C1 moved by one ulp (config2_reference_order_ulp.json) leaves 1e-10 at the same iteration as
+    the contract mode does (20) and changes its iteration count by MORE (513 -> 480) than the
+    contract mode differs from it (520 vs 513): the contract's distance from the reference order
+    is inside the reference's own rounding sensitivity."""
+    ref, ulp, rep = load(2, "reference_order"), load(2, "reference_order_ulp"), load(2, "reproducible")
+    assert ulp["perturbed"] and ulp["status"] == ref["status"] == rep["status"] == "converged"
+
+    def first_above(x, y, thr):
+        n = min(len(x), len(y))
+        d = np.abs(np.array(x[:n]) - np.array(y[:n])) / np.abs(np.array(y[:n]))
+        return int(np.argmax(d > thr))
+
+    i_self = first_above(ulp["rel_residual"], ref["rel_residual"], 1e-10)
+    i_rep = first_above(rep["rel_residual"], ref["rel_residual"], 1e-10)
+    assert abs(i_self - i_rep) <= 4, (i_self, i_rep)
+    assert abs(ulp["iterations"] - ref["iterations"]) >= abs(rep["iterations"] - ref["iterations"])
