@@ -30,7 +30,7 @@ BICG_WINDOW = {2: 12, 4: 12}
 # iteration-count slack: the reference-order run's own spread under a one-ulp input change
 # (tests/golden/config*_reference_order_ulp*.json; C4: reproducible 197, reference order 168,
 # reference order with C1 scaled by 1 + 2^-52: 187; C2: 520 / 513 / 480)
-BICG_COUNT_SLACK = {2: 33, 4: 38}  # twice... no: the measured self-spread (33 at C2) and 2 x 19 at C4
+BICG_COUNT_SLACK = {2: 33, 4: 38}  # the measured self-spread at C2 (33) and twice it at C4 (2 x 19)
 
 
 def golden(idx, mode):
